@@ -1,0 +1,163 @@
+// bb_common.cuh -- shared device/host helpers for the B200 binbatch engine.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <math_constants.h>
+
+#include "binbatch_b200.h"
+
+#define BB_HD __host__ __device__ __forceinline__
+
+namespace bb {
+
+// host-side launch accounting (bb_launch_count)
+void note_launch(unsigned n = 1);
+
+// ----------------------------------------------------------------- Philox
+// Philox4x32-10 (Salmon et al., SC'11).  Replaces the reference's sequential
+// std::mt19937_64 streams (rng.hpp:28-53) with a counter-based generator so
+// any (request, stream, replica seed) draw is computable independently.
+// Constants and KATs: SURVEY App. C; curand_philox4x32_x.h:88-91.
+constexpr uint32_t kPhiloxM0 = 0xD2511F53u, kPhiloxM1 = 0xCD9E8D57u;
+constexpr uint32_t kPhiloxW0 = 0x9E3779B9u, kPhiloxW1 = 0xBB67AE85u;
+// The engine's fixed key; streams are separated through the counter
+// (c1 = stream id, c2:c3 = whitened replica seed), so the key can be a
+// compile-time constant folded into every round.
+constexpr uint32_t kKey0 = 0xA4093822u, kKey1 = 0x299F31D0u;
+
+BB_HD uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+#ifdef __CUDA_ARCH__
+    const uint32_t hi0 = __umulhi(kPhiloxM0, c.x), lo0 = kPhiloxM0 * c.x;
+    const uint32_t hi1 = __umulhi(kPhiloxM1, c.z), lo1 = kPhiloxM1 * c.z;
+#else
+    const uint64_t p0 = (uint64_t)kPhiloxM0 * c.x, p1 = (uint64_t)kPhiloxM1 * c.z;
+    const uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+    const uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+#endif
+    c = make_uint4(hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0);
+    k0 += kPhiloxW0;
+    k1 += kPhiloxW1;
+  }
+  return c;
+}
+
+BB_HD uint4 philox(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3) {
+  return philox4x32_10(make_uint4(c0, c1, c2, c3), kKey0, kKey1);
+}
+
+// 53-bit integer from two 32-bit words; u = x * 2^-53 is the reference's
+// uniform01 resolution (rng.hpp:38).
+BB_HD uint64_t bits53(uint32_t hi, uint32_t lo) { return ((uint64_t)hi << 21) | (lo >> 11); }
+
+constexpr uint64_t kKeyDomain53 = 1ull << 53;
+
+// detail::splitmix64, rng.hpp:16-21
+BB_HD uint64_t splitmix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+// replication_seed, experiment.hpp:90-92
+BB_HD uint64_t replication_seed(uint64_t master, uint64_t rep) {
+  return splitmix64(master ^ splitmix64(rep + 0x51ED2701A7B4E5D3ull));
+}
+
+// Stream ids (Philox counter word c1).
+enum : uint32_t { kStreamArrivalService = 0, kStreamError = 1 };
+
+// --------------------------------------------------------- service in key space
+// Generated mode draws a 53-bit key x per request and the service time is a
+// monotone non-decreasing function s(x).  Bins are therefore thresholds on x
+// (found by bisection on the same device function), and a batch's service
+// max_i s(x_i) == s(max_i x_i): the transcendental runs once per batch.
+enum SvcKind : int32_t {
+  kSvcUniform = 0,   // lo + (hi-lo)*u                 (rng.hpp:40)
+  kSvcExponential,   // -log1p(-u)/rate                (rng.hpp:43)
+  kSvcLogNormal,     // exp(mu + sigma*Phi^-1(u'))     u' = (x+1/2)*2^-53
+  kSvcTable,         // sorted[floor(u*n)]             (service_dist.hpp:98)
+  kSvcLinear,        // b*(lo + (hi-lo)*u) + a         (workload.hpp:167-170)
+  kSvcCyclic         // sorted[x], x = rank of lengths[id % n] (simulator.hpp:350)
+};
+
+struct SvcParams {
+  int32_t kind;
+  uint32_t n_table;
+  double lo, hi, rate, mu, sigma, lin_a, lin_b;
+  const double* table;   // sorted ascending (device)
+  uint64_t key_domain;   // 2^53, or n_table for cyclic
+};
+
+__device__ __forceinline__ double svc_of_key(const SvcParams& p, uint64_t x) {
+  switch (p.kind) {
+    case kSvcUniform: {
+      const double u = (double)x * 0x1.0p-53;
+      return __dadd_rn(p.lo, __dmul_rn(__dsub_rn(p.hi, p.lo), u));
+    }
+    case kSvcLinear: {
+      const double u = (double)x * 0x1.0p-53;
+      const double len = __dadd_rn(p.lo, __dmul_rn(__dsub_rn(p.hi, p.lo), u));
+      return __dadd_rn(__dmul_rn(p.lin_b, len), p.lin_a);
+    }
+    case kSvcExponential: {
+      const double u = (double)x * 0x1.0p-53;
+      return -log1p(-u) / p.rate;
+    }
+    case kSvcLogNormal: {
+      const double u = ((double)x + 0.5) * 0x1.0p-53;
+      return exp(p.mu + p.sigma * normcdfinv(u));
+    }
+    case kSvcTable: {
+      const uint64_t idx = __umul64hi(x << 11, (uint64_t)p.n_table);
+      return p.table[idx];
+    }
+    default:  // kSvcCyclic
+      return p.table[x];
+  }
+}
+
+// ------------------------------------------------------------- errors
+// First failing request wins (the reference throws at the first offending
+// arrival in event order): packed (index << 8 | code) via atomicMin.
+struct DevError {
+  unsigned long long packed;  // UINT64_MAX == no error
+  double value;               // offending value (for the message)
+  unsigned long long aux;     // replica / extra
+};
+
+__device__ __forceinline__ void raise_error(DevError* e, uint64_t index, int code, double value,
+                                            uint64_t aux = 0) {
+  const unsigned long long p = ((unsigned long long)index << 8) | (unsigned)code;
+  const unsigned long long old = atomicMin(&e->packed, p);
+  if (p < old) {
+    e->value = value;  // best effort (racy only among failing threads)
+    e->aux = aux;
+  }
+}
+
+// ------------------------------------------------------ fast 32-bit divider
+// n / d for runtime d via one mul-hi (Granlund-Montgomery); exact for all
+// 32-bit n.
+struct FastDiv {
+  uint32_t d, m, s;
+  BB_HD FastDiv() : d(1), m(0), s(0) {}
+  BB_HD explicit FastDiv(uint32_t dv) : d(dv) {
+    uint32_t l = 0;
+    while (l < 32 && (1ull << l) < dv) ++l;
+    s = l;
+    m = (uint32_t)((((1ull << 32) * ((1ull << l) - dv)) / dv) + 1);
+  }
+  BB_HD uint32_t div(uint32_t n) const {
+#ifdef __CUDA_ARCH__
+    const uint64_t t = (uint64_t)__umulhi(n, m) + n;
+#else
+    const uint64_t t = (((uint64_t)n * m) >> 32) + n;
+#endif
+    return (uint32_t)(t >> s);
+  }
+};
+
+}  // namespace bb

@@ -1,0 +1,417 @@
+// bb_generated.cu -- generated-mode Monte Carlo engine (K1 + K7 + K6 of SURVEY §2.3).
+//
+// One thread simulates one replication end to end, a warp owns 32
+// replications of one sweep point, and a persistent grid walks the
+// (point, 32-replication chunk) work list.  Per request the thread draws one
+// Philox4x32-10 block (53-bit inter-arrival uniform + 53-bit service key),
+// assigns the bin in key space, folds the request into its bin's packed
+// (max key, count) word in shared memory and, when the bin reaches B, closes
+// the batch with the single-server Lindley step
+//     D = max(D, R) + S,  R = arrival of the closing request
+// (simulator.hpp:256-267 with one server).  Nothing per request
+// touches HBM: the kernel is SM-issue bound.
+//
+// Dispatch semantics reproduced:
+//   finite lambda -- batches dispatch in closing-request order, then the
+//     final partials in bin order 1..k (drain events, simulator.hpp:203-205);
+//   overload -- one tie group: round 0 in first-closing order, then either
+//     round-robin rounds (no flush) or per-bin drains (flush).  Positions are
+//     closed-form from a first counting pass; the second pass replays the
+//     same counter-based draws.
+#include "bb_generated.cuh"
+
+namespace bb {
+namespace {
+
+constexpr int kGenThreads = 256;
+constexpr int kGenWarps = kGenThreads / 32;
+constexpr uint64_t kCntBits = 11;
+constexpr uint64_t kCntMask = (1ull << kCntBits) - 1;  // B <= 2047 in the packed state
+
+__global__ void thresholds_kernel(GenPoint* pts, uint32_t n_points) {
+  const uint32_t p = blockIdx.x;
+  if (p >= n_points) return;
+  GenPoint& P = pts[p];
+  const uint32_t k = P.k;
+  const uint64_t D = P.svc.key_domain;
+  __shared__ uint64_t s_pos, s_above;
+  for (uint32_t j = threadIdx.x; j <= k + 2; j += blockDim.x) {
+    // smallest key whose service satisfies the predicate (monotone in the key)
+    uint64_t lo = 0, hi = D;
+    while (lo < hi) {
+      const uint64_t mid = lo + (hi - lo) / 2;
+      const double s = svc_of_key(P.svc, mid);
+      bool ok;
+      if (j <= k) ok = s >= P.edges[j];       // e_j <= s   (assign_bin upper_bound)
+      else if (j == k + 1) ok = s > 0.0;      // positive   (simulator.hpp:189)
+      else ok = s > P.edges[k];               // above the top edge (binning.hpp:135)
+      if (ok) hi = mid;
+      else lo = mid + 1;
+    }
+    if (j <= k) P.thr[j] = lo;
+    else if (j == k + 1) s_pos = lo;
+    else s_above = lo;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint64_t vlo = P.thr[0] > s_pos ? P.thr[0] : s_pos;
+    if (s_above == 0) {  // every key is above the support
+      P.vlo = 1;
+      P.vhi = 0;
+      P.check_domain = 1;
+    } else {
+      P.vlo = vlo;
+      P.vhi = s_above - 1;
+      P.check_domain = !(vlo == 0 && s_above == D);
+    }
+  }
+}
+
+// 1 + #{j in 1..k-1 : thr[j] <= x}  (== assign_bin for monotone s(x))
+__device__ __forceinline__ uint32_t bin_of(const uint64_t* thr, uint32_t k, uint32_t top,
+                                           uint64_t x) {
+  uint32_t pos = 0;
+  for (uint32_t step = top; step; step >>= 1)
+    if (pos + step < k && thr[pos + step] <= x) pos += step;
+  return pos + 1;
+}
+
+// predict_bin, binning.hpp:231-261, in key space of the error uniform
+template <int ERR>
+__device__ __forceinline__ uint32_t predict(const GenPoint& P, uint32_t tb, uint32_t k,
+                                            uint64_t xe) {
+  if (ERR == 1) {
+    if (tb == 1) return xe < P.e_t1 ? 2u : 1u;
+    if (tb == k) return xe < P.e_t1 ? k - 1 : k;
+    if (xe < P.e_t1) return tb - 1;
+    if (xe >= P.e_t2) return tb + 1;
+    return tb;
+  } else if (ERR == 2) {
+    const uint64_t* row = P.conf_thr + (uint64_t)(tb - 1) * k;
+    uint32_t pb = 1;
+    for (uint32_t j = 0; j + 1 < k; ++j) pb += xe >= row[j];
+    return pb;
+  }
+  return tb;
+}
+
+struct Draw {
+  uint64_t xg;  // inter-arrival uniform (53-bit)
+  uint64_t xs;  // service key
+  uint64_t xe;  // error uniform (53-bit)
+};
+
+template <int ERR, bool CYC>
+__device__ __forceinline__ Draw draw(const GenPoint& P, uint32_t i, uint32_t c2, uint32_t c3,
+                                     uint4& ecache, uint32_t& cyc) {
+  Draw d;
+  const uint4 r = philox(i, kStreamArrivalService, c2, c3);
+  d.xg = bits53(r.x, r.y);
+  if (CYC) {
+    d.xs = P.cyc_rank[cyc];
+    if (++cyc == P.svc.n_table) cyc = 0;
+  } else {
+    d.xs = bits53(r.z, r.w);
+  }
+  d.xe = 0;
+  if (ERR != 0) {
+    if ((i & 1u) == 0) ecache = philox(i >> 1, kStreamError, c2, c3);
+    d.xe = (i & 1u) ? bits53(ecache.z, ecache.w) : bits53(ecache.x, ecache.y);
+  }
+  return d;
+}
+
+template <int ERR, bool CYC, bool OVL>
+__global__ void __launch_bounds__(kGenThreads) gen_kernel(GenLaunch L) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ uint64_t s_thr[kGenWarps][BB_MAX_BINS + 1];
+  const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5, tid = threadIdx.x;
+  const uint32_t kmax = L.k_max;
+  uint64_t* st = reinterpret_cast<uint64_t*>(smem_raw);  // [kmax][T] packed (key<<11 | cnt)
+  double* s_osum = reinterpret_cast<double*>(st + (size_t)kmax * kGenThreads);  // finite, no flush
+  uint32_t* s_F = reinterpret_cast<uint32_t*>(st + (size_t)kmax * kGenThreads);  // overload
+  uint32_t* s_rem = s_F + (size_t)kmax * kGenThreads;
+  uint32_t* s_cf = s_rem + (size_t)kmax * kGenThreads;
+  uint32_t* s_jd = s_cf + (size_t)kmax * kGenThreads;
+
+  const uint32_t nrep = L.rep_end - L.rep_begin;
+  const uint32_t chunks = (nrep + 31) / 32;
+  const uint64_t n_items = (uint64_t)chunks * L.n_points;
+  const uint64_t stride = (uint64_t)L.points_total * L.reps_total;
+  const uint64_t gwarp = (uint64_t)blockIdx.x * kGenWarps + wib;
+  const uint64_t nwarps = (uint64_t)gridDim.x * kGenWarps;
+
+  for (uint64_t w = gwarp; w < n_items; w += nwarps) {
+    const uint32_t p = (uint32_t)(w / chunks), c = (uint32_t)(w % chunks);
+    const GenPoint& P = L.pts_dev[p];
+    const uint32_t k = P.k, B = P.B, n = P.n;
+    for (uint32_t j = lane; j <= k; j += 32) s_thr[wib][j] = P.thr[j];
+    __syncwarp();
+    const uint32_t r = L.rep_begin + c * 32 + lane;
+    if (r < L.rep_end) {
+      const uint64_t seed = L.single_seed ? L.master : replication_seed(L.master, r);
+      const uint64_t sw = splitmix64(seed);  // RandomStream(seed) whitening, rng.hpp:30
+      const uint32_t c2 = (uint32_t)sw, c3 = (uint32_t)(sw >> 32);
+      const uint64_t* thr = s_thr[wib];
+      const uint32_t top = k > 1 ? (1u << (31 - __clz(k - 1))) : 0u;
+      const bool check = P.check_domain != 0;
+      const uint64_t vlo = P.vlo, vhi = P.vhi;
+      const bool flush = P.flush != 0;
+      for (uint32_t b = 0; b < k; ++b) st[b * kGenThreads + tid] = 0;
+      uint4 ecache = make_uint4(0, 0, 0, 0);
+      uint32_t cyc = 0;
+      bool failed = false;
+      double thr_out, lat_out, mk_out, busy_out;
+
+      if (!OVL) {
+        // ------------------------------------------------ finite arrival rate
+        const double inv_lambda = P.inv_lambda;
+        const bool track = !flush;
+        if (track)
+          for (uint32_t b = 0; b < k; ++b) s_osum[b * kGenThreads + tid] = 0.0;
+        double t = 0.0, D = 0.0, busy = 0.0, latw = 0.0, asum = 0.0, a0 = 0.0;
+        uint64_t ncomp = 0;
+        for (uint32_t i = 0; i < n; ++i) {
+          const Draw d = draw<ERR, CYC>(P, i, c2, c3, ecache, cyc);
+          // exponential inter-arrival, rng.hpp:43 / simulator.hpp:181
+          t += -log1p(-(double)d.xg * 0x1.0p-53) * inv_lambda;
+          asum += t;
+          if (i == 0) a0 = t;
+          if (check && (d.xs < vlo || d.xs > vhi)) {
+            raise_error(L.err, i, BB_EDOMAIN, svc_of_key(P.svc, d.xs), r);
+            failed = true;
+            break;
+          }
+          const uint32_t tb = k > 1 ? bin_of(thr, k, top, d.xs) : 1u;
+          const uint32_t pb = ERR ? predict<ERR>(P, tb, k, d.xe) : tb;
+          uint64_t* slot = st + (pb - 1) * kGenThreads + tid;
+          const uint64_t s0 = *slot;
+          const uint64_t km = max(s0 & ~kCntMask, d.xs << kCntBits);
+          const uint32_t cnt = (uint32_t)(s0 & kCntMask) + 1;
+          if (cnt == B) {  // form_batch + dispatch, simulator.hpp:237-267
+            *slot = 0;
+            const double S = svc_of_key(P.svc, km >> kCntBits);
+            D = __dadd_rn(fmax(D, t), S);
+            busy += S;
+            latw += (double)B * D;
+            ncomp += B;
+            if (track) s_osum[(pb - 1) * kGenThreads + tid] = 0.0;
+          } else {
+            *slot = km | cnt;
+            if (track) s_osum[(pb - 1) * kGenThreads + tid] += t;
+          }
+        }
+        double leftover = 0.0;
+        if (!failed) {
+          for (uint32_t b = 0; b < k; ++b) {
+            const uint64_t s0 = st[b * kGenThreads + tid];
+            const uint32_t cnt = (uint32_t)(s0 & kCntMask);
+            if (!cnt) continue;
+            if (flush) {  // on_drain partials at the last arrival, bin order
+              const double S = svc_of_key(P.svc, s0 >> kCntBits);
+              D = __dadd_rn(fmax(D, t), S);
+              busy += S;
+              latw += (double)cnt * D;
+              ncomp += cnt;
+            } else {
+              leftover += s_osum[b * kGenThreads + tid];
+            }
+          }
+        }
+        if (!failed && ncomp > 0) {  // finish(), simulator.hpp:279-301
+          mk_out = D - a0;
+          thr_out = (double)ncomp / mk_out;
+          busy_out = busy / mk_out;
+          lat_out = (latw - (asum - leftover)) / (double)ncomp;
+        } else {
+          mk_out = thr_out = busy_out = lat_out = failed ? CUDART_NAN : 0.0;
+        }
+      } else {
+        // ------------------------------------------------------- overload
+        for (uint32_t b = 0; b < k; ++b) {
+          s_F[b * kGenThreads + tid] = 0;
+          s_cf[b * kGenThreads + tid] = 0xFFFFFFFFu;
+        }
+        for (uint32_t i = 0; i < n; ++i) {  // pass 1: per-bin totals, first closings
+          const Draw d = draw<ERR, CYC>(P, i, c2, c3, ecache, cyc);
+          if (check && (d.xs < vlo || d.xs > vhi)) {
+            raise_error(L.err, i, BB_EDOMAIN, svc_of_key(P.svc, d.xs), r);
+            failed = true;
+            break;
+          }
+          const uint32_t tb = k > 1 ? bin_of(thr, k, top, d.xs) : 1u;
+          const uint32_t pb = ERR ? predict<ERR>(P, tb, k, d.xe) : tb;
+          const uint32_t cnt = ++s_F[(pb - 1) * kGenThreads + tid];
+          if (cnt == B) s_cf[(pb - 1) * kGenThreads + tid] = i;
+        }
+        if (!failed) {
+          uint32_t Z = 0;
+          uint64_t nc = 0;
+          for (uint32_t b = 0; b < k; ++b) {
+            const uint32_t cnt = s_F[b * kGenThreads + tid];
+            const uint32_t F = cnt / B, rem = cnt - F * B;
+            s_F[b * kGenThreads + tid] = F;
+            s_rem[b * kGenThreads + tid] = rem;
+            s_jd[b * kGenThreads + tid] = 0;
+            Z += F >= 1;
+            nc += (uint64_t)F * B + (flush ? rem : 0);
+          }
+          cyc = 0;
+          double busy = 0.0, latw = 0.0;
+          for (uint32_t i = 0; i < n; ++i) {  // pass 2: same draws, batch positions
+            const Draw d = draw<ERR, CYC>(P, i, c2, c3, ecache, cyc);
+            const uint32_t tb = k > 1 ? bin_of(thr, k, top, d.xs) : 1u;
+            const uint32_t pb = ERR ? predict<ERR>(P, tb, k, d.xe) : tb;
+            uint64_t* slot = st + (pb - 1) * kGenThreads + tid;
+            const uint64_t s0 = *slot;
+            const uint64_t km = max(s0 & ~kCntMask, d.xs << kCntBits);
+            const uint32_t cnt = (uint32_t)(s0 & kCntMask) + 1;
+            if (cnt == B) {
+              *slot = 0;
+              const uint32_t b = pb - 1;
+              const uint32_t j = s_jd[b * kGenThreads + tid]++;
+              const uint32_t cfb = s_cf[b * kGenThreads + tid];
+              uint64_t before;
+              if (flush && j > 0) {  // drain phase, bins in order
+                before = (uint64_t)B * Z + (uint64_t)B * (j - 1);
+                for (uint32_t q = 0; q < b; ++q) {
+                  const uint32_t F = s_F[q * kGenThreads + tid];
+                  before += (uint64_t)B * (F ? F - 1 : 0) + s_rem[q * kGenThreads + tid];
+                }
+              } else {  // round j, first-closing order
+                uint64_t pos = 0;
+                for (uint32_t q = 0; q < k; ++q) {
+                  const uint32_t F = s_F[q * kGenThreads + tid];
+                  const uint32_t cq = s_cf[q * kGenThreads + tid];
+                  if (!flush) pos += F < j ? F : j;
+                  pos += (cq < cfb) && (F > j);
+                }
+                before = (uint64_t)B * pos;
+              }
+              const double S = svc_of_key(P.svc, km >> kCntBits);
+              busy += S;
+              latw += S * (double)(nc - before);
+            } else {
+              *slot = km | cnt;
+            }
+          }
+          if (flush) {
+            uint64_t base = (uint64_t)B * Z;
+            for (uint32_t b = 0; b < k; ++b) {
+              const uint32_t F = s_F[b * kGenThreads + tid];
+              const uint32_t rem = s_rem[b * kGenThreads + tid];
+              base += (uint64_t)B * (F ? F - 1 : 0);
+              if (rem) {
+                const double S = svc_of_key(P.svc, st[b * kGenThreads + tid] >> kCntBits);
+                busy += S;
+                latw += S * (double)(nc - base);
+              }
+              base += rem;
+            }
+          }
+          if (nc > 0) {
+            mk_out = busy;  // all requests arrive at t=0 and the server never idles
+            thr_out = (double)nc / mk_out;
+            busy_out = busy / mk_out;
+            lat_out = latw / (double)nc;
+          } else {
+            mk_out = thr_out = busy_out = lat_out = 0.0;
+          }
+        } else {
+          mk_out = thr_out = busy_out = lat_out = CUDART_NAN;
+        }
+      }
+      const uint64_t o = (uint64_t)P.gidx * L.reps_total + r;
+      L.out[BB_REP_THROUGHPUT * stride + o] = thr_out;
+      L.out[BB_REP_LATENCY * stride + o] = lat_out;
+      L.out[BB_REP_P50 * stride + o] = CUDART_NAN;  // generated mode: not tracked (SURVEY §7 hard part 4)
+      L.out[BB_REP_P99 * stride + o] = CUDART_NAN;
+      L.out[BB_REP_MAKESPAN * stride + o] = mk_out;
+      L.out[BB_REP_BUSY * stride + o] = busy_out;
+    }
+    __syncwarp();
+  }
+}
+
+// mean_std (experiment.hpp:188-200) in replica order, bit-for-bit the
+// reference's sequential sums.  One block per point, one thread per field.
+__global__ void point_reduce_kernel(const double* __restrict__ rep, uint32_t n_points,
+                                    uint32_t reps, double* __restrict__ out) {
+  const uint32_t p = blockIdx.x, f = threadIdx.x;
+  if (p >= n_points || f >= BB_REP_FIELDS) return;
+  const uint64_t stride = (uint64_t)n_points * reps;
+  const double* x = rep + f * stride + (uint64_t)p * reps;
+  const double nn = (double)reps;
+  double sum = 0;
+  for (uint32_t i = 0; i < reps; ++i) sum += x[i];
+  const double mean = sum / nn;
+  double sd = 0;
+  if (reps >= 2 && (f == BB_REP_THROUGHPUT || f == BB_REP_LATENCY)) {
+    double ss = 0;
+    for (uint32_t i = 0; i < reps; ++i) ss += (x[i] - mean) * (x[i] - mean);
+    sd = sqrt(ss / (nn - 1.0));
+  }
+  double* o = out + (uint64_t)p * 8;
+  switch (f) {
+    case BB_REP_THROUGHPUT: o[0] = mean; o[1] = sd; break;
+    case BB_REP_LATENCY: o[2] = mean; o[3] = sd; break;
+    case BB_REP_P50: o[4] = mean; break;
+    case BB_REP_P99: o[5] = mean; break;
+    case BB_REP_MAKESPAN: o[6] = mean; break;
+    case BB_REP_BUSY: o[7] = mean; break;
+  }
+}
+
+template <int ERR, bool CYC, bool OVL>
+cudaError_t launch_gen(const GenLaunch& L, cudaStream_t s) {
+  const size_t per = OVL ? (8 + 16) : 16;  // packed state + open sums | overload tables
+  const size_t smem = (size_t)L.k_max * kGenThreads * per;
+  auto kern = gen_kernel<ERR, CYC, OVL>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 0, occ = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kGenThreads, smem);
+  if (e != cudaSuccess) return e;
+  if (occ < 1) return cudaErrorInvalidConfiguration;
+  const uint32_t nrep = L.rep_end - L.rep_begin;
+  const uint64_t items = (uint64_t)((nrep + 31) / 32) * L.n_points;
+  const uint64_t want = (items + kGenWarps - 1) / kGenWarps;
+  const uint64_t cap = (uint64_t)sms * occ;
+  const unsigned grid = (unsigned)(want < cap ? want : cap);
+  if (grid == 0) return cudaSuccess;
+  kern<<<grid, kGenThreads, smem, s>>>(L);
+  note_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t gen_setup_thresholds(GenPoint* pts_dev, uint32_t n_points, cudaStream_t s) {
+  if (!n_points) return cudaSuccess;
+  thresholds_kernel<<<n_points, 64, 0, s>>>(pts_dev, n_points);
+  note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t gen_run(const GenLaunch& L, cudaStream_t s) {
+#define BB_GEN_CASE(E, C, O) \
+  if (L.err_kind == E && (L.cyclic != 0) == C && (L.overload != 0) == O) return launch_gen<E, C, O>(L, s);
+  BB_GEN_CASE(0, false, false) BB_GEN_CASE(1, false, false) BB_GEN_CASE(2, false, false)
+  BB_GEN_CASE(0, true, false) BB_GEN_CASE(1, true, false) BB_GEN_CASE(2, true, false)
+  BB_GEN_CASE(0, false, true) BB_GEN_CASE(1, false, true) BB_GEN_CASE(2, false, true)
+  BB_GEN_CASE(0, true, true) BB_GEN_CASE(1, true, true) BB_GEN_CASE(2, true, true)
+#undef BB_GEN_CASE
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t gen_point_reduce(const double* rep, uint32_t n_points, uint32_t reps, double* stats,
+                             cudaStream_t s) {
+  if (!n_points) return cudaSuccess;
+  point_reduce_kernel<<<n_points, 32, 0, s>>>(rep, n_points, reps, stats);
+  note_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace bb

@@ -1,0 +1,50 @@
+// bb_generated.cuh -- generated-mode (Philox) engine interface.
+#pragma once
+#include "bb_common.cuh"
+
+namespace bb {
+
+// One sweep point, flattened for the device (materialize(),
+// experiment.hpp:110-155, resolved to key space).
+struct GenPoint {
+  SvcParams svc;
+  double inv_lambda;        // 0 => overload (kOverload, simulator.hpp:33)
+  uint32_t n, B, k;
+  uint32_t flush;           // flush_partial
+  uint32_t err_kind;        // 0 perfect, 1 symmetric, 2 confusion
+  uint32_t check_domain;    // keys outside [vlo, vhi] raise domain_error
+  uint32_t gidx;            // global point index (output row)
+  uint64_t vlo, vhi;
+  uint64_t e_t1, e_t2;      // symmetric: u < p <=> x < t1 ; u >= 1-p <=> x >= t2
+  const double* edges;      // k+1 (device), input of the threshold setup
+  const uint64_t* conf_thr; // confusion: k*k cumulative thresholds (device)
+  const uint32_t* cyc_rank; // cyclic: sorted rank of lengths[j] (device)
+  uint64_t thr[BB_MAX_BINS + 1];  // thr[j], j=1..k-1: bin > j <=> x >= thr[j]
+};
+
+struct GenLaunch {
+  const GenPoint* pts_dev;  // n_points (thresholds already resolved)
+  uint32_t n_points;        // points in this launch
+  uint32_t points_total;    // rows of the output array
+  uint32_t k_max;
+  uint64_t master;          // run_point master seed; replica seed = replication_seed(master, r)
+  int32_t single_seed;      // 1: replica 0 uses `master` itself as the seed (run_simulation)
+  uint32_t reps_total;      // replications per point (array stride)
+  uint32_t rep_begin, rep_end;
+  int32_t err_kind;
+  int32_t cyclic;
+  int32_t overload;
+  double* out;              // [BB_REP_FIELDS][n_points*reps_total]
+  DevError* err;
+};
+
+// Resolves key-space thresholds (bisection on the device sampler).
+cudaError_t gen_setup_thresholds(GenPoint* pts_dev, uint32_t n_points, cudaStream_t s);
+// The fused per-replica kernel.  Returns the launch error.
+cudaError_t gen_run(const GenLaunch& L, cudaStream_t s);
+// mean_std per point over replica order (experiment.hpp:188-200, :275-281).
+// stats_out: [n_points][8] = thr mean, thr std, lat mean, lat std, p50, p99, makespan, busy
+cudaError_t gen_point_reduce(const double* rep, uint32_t n_points, uint32_t reps,
+                             double* stats_out, cudaStream_t s);
+
+}  // namespace bb

@@ -1,0 +1,1136 @@
+// bb_trace.cu -- trace-mode pipeline: the reference engine's results,
+// bit-for-bit, from given request streams.
+//
+//   K2 partition_kernel   one pass over the requests (decoupled look-back):
+//        service check + assign_bin + predict_bin            binning.hpp:133-144, :231-261
+//        stable per-bin rank (warp ballots, k-vector look-back) simulator.hpp:196-197
+//        batch service = max over the B members (fragment maxima in smem,
+//          open-batch max carried across tiles by a 2nd look-back) :237-254
+//        closing records in closing-request order (R = closing arrival)   :198-199
+//   finalize / order      drain partials, dispatch order (App. A.2)      :203-221
+//   K5 Lindley            D = fl(max(D,R) + S): max-plus scan -> certified
+//                         busy-period splits -> exact serial segments   :256-277
+//   K6 request pass       completion, latency, sum, quantile keys        :279-301
+//   select                exact order statistics for p50/p99 (radix refine)
+//
+// HBM layout: inputs a[], s[] (fp64, 8 B/request) and pred[] (u8) or u_err[]
+// (fp64); per-request scratch pb8 (u8) + rank (u32); per-batch SoA records.
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "bb_trace.cuh"
+
+namespace bb {
+namespace {
+
+constexpr int TB = 256, IPT = 8, TILE = TB * IPT, NW = TB / 32;
+constexpr unsigned long long FLAG_A = 1ull << 62, FLAG_P = 2ull << 62, VAL_MASK = (1ull << 62) - 1;
+constexpr unsigned long long KEY_UNSERVED = ~0ull;
+constexpr uint32_t FL_NONMONO = 1, FL_TIE_GT_B = 2, FL_NOT_ALL_EQUAL = 4;
+constexpr int LB = 256, LI = 8, LTILE = LB * LI;  // Lindley scan tile
+constexpr int HBITS = 12, HBINS = 1 << HBITS;
+
+__device__ __forceinline__ void st_release64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release32(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long ld_relaxed64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// Per-run facts computed on the device by finalize_kernel and read back.
+struct Info {
+  uint32_t nclose, nb, npartial, Z, path, flags;
+  unsigned long long nc;
+  uint32_t F[BB_TRACE_MAX_BINS], rem[BB_TRACE_MAX_BINS], nbat[BB_TRACE_MAX_BINS];
+  uint32_t bin_base[BB_TRACE_MAX_BINS];   // first map slot of bin b
+  uint32_t dbase[BB_TRACE_MAX_BINS];      // overload+flush: drain position base of bin b
+  unsigned long long dreq[BB_TRACE_MAX_BINS];  // overload+flush: requests before bin b's drain
+  uint32_t pfirst[BB_TRACE_MAX_BINS];     // fast path: members offset of bin b's partial
+  uint32_t cfirst[BB_TRACE_MAX_BINS];     // overload: closing index of batch (b,0)
+};
+
+struct WS {
+  uint32_t* counters;            // [0] partition tiles, [1] lindley tiles
+  unsigned long long* desc1;     // [ntiles*k] flag|count
+  unsigned long long* desc2v;    // [ntiles*k] alpha<<63 | open-max bits
+  uint32_t* desc2f;              // [ntiles*k]
+  uint8_t* pb8;
+  uint32_t* rank;
+  double *recR, *recS;
+  uint8_t* recBin;
+  uint32_t *recJ, *recC;
+  unsigned long long* fin_cnt;   // [k]
+  unsigned long long* fin_open;  // [k] double bits
+  uint32_t* flags;
+  DevError* err;
+  Info* info;
+};
+
+struct PartArgs {
+  const double* a;
+  const double* s;
+  const double* u_err;
+  const uint8_t* pred;
+  const double* edges;
+  const double* conf;
+  uint8_t* tb_out;
+  uint32_t n, B, k, ntiles;
+  int32_t err_kind;
+  double p, one_minus_p;
+  FastDiv divB;
+  WS ws;
+};
+
+// assign_bin, binning.hpp:133-144 (0 = out of support)
+__device__ __forceinline__ uint32_t assign_bin(const double* e, uint32_t k, double len) {
+  if (!(len >= e[0]) || !(len <= e[k])) return 0;
+  if (len == e[k]) return k;
+  uint32_t lo = 1, hi = k;  // first index in [1,k] with e[idx] > len
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (e[mid] > len) hi = mid;
+    else lo = mid + 1;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(TB) partition_kernel(PartArgs P) {
+  __shared__ double s_edges[BB_TRACE_MAX_BINS + 1];
+  __shared__ uint32_t s_wcnt[NW][32], s_woff[NW][32];
+  __shared__ uint32_t s_excl[32], s_tot[32], s_jlo[32], s_fbase[32], s_nfrag[32];
+  __shared__ unsigned long long s_slot[TILE + 32];
+  __shared__ uint32_t s_wclose[NW];
+  __shared__ uint32_t s_closebase, s_tile, s_flags, s_nfrag_total;
+
+  const uint32_t tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const uint32_t k = P.k, n = P.n, B = P.B;
+  if (tid == 0) {
+    s_tile = atomicAdd(&P.ws.counters[0], 1u);
+    s_flags = 0;
+  }
+  for (uint32_t i = tid; i <= k; i += TB) s_edges[i] = P.edges[i];
+  __syncthreads();
+  const uint32_t t = s_tile;
+  const uint64_t wbase = (uint64_t)t * TILE + w * (32 * IPT);
+
+  double av[IPT], sv[IPT];
+  uint32_t pb[IPT], rl[IPT];
+#pragma unroll
+  for (int j = 0; j < IPT; ++j) {
+    const uint64_t idx = wbase + j * 32 + lane;
+    av[j] = idx < n ? P.a[idx] : 0.0;
+    sv[j] = idx < n ? P.s[idx] : 0.0;
+  }
+  const double a0 = P.a[0];
+  uint32_t flags = 0;
+#pragma unroll
+  for (int j = 0; j < IPT; ++j) {
+    const uint64_t idx = wbase + j * 32 + lane;
+    const bool valid = idx < n;
+    // predecessor arrival for the monotonicity / tie checks
+    double prev = __shfl_up_sync(0xffffffffu, av[j], 1);
+    const double prevj = __shfl_sync(0xffffffffu, av[j > 0 ? j - 1 : 0], 31);
+    if (lane == 0) prev = j > 0 ? prevj : (idx > 0 && valid ? P.a[idx - 1] : av[j]);
+    uint32_t tb = 0, b = 0;
+    if (valid) {
+      if (idx > 0) {
+        if (!(av[j] >= prev)) flags |= FL_NONMONO;
+        else if (av[j] == prev && idx >= B && P.a[idx - B] == av[j]) flags |= FL_TIE_GT_B;
+      }
+      if (av[j] != a0) flags |= FL_NOT_ALL_EQUAL;
+      const double s = sv[j];
+      if (!(s > 0) || !isfinite(s)) {
+        raise_error(P.ws.err, idx, BB_EDOMAIN, s, 1);  // simulator.hpp:189-190
+      } else if ((tb = assign_bin(s_edges, k, s)) == 0) {
+        raise_error(P.ws.err, idx, BB_EDOMAIN, s, 2);  // binning.hpp:135-140
+      } else if (P.pred) {
+        b = P.pred[idx];
+        if (b < 1 || b > k) {
+          raise_error(P.ws.err, idx, BB_EINVAL, (double)b, 3);
+          b = 0;
+        }
+      } else if (P.err_kind == 1) {  // Symmetric, binning.hpp:238-246
+        const double u = P.u_err[idx];
+        if (tb == 1) b = u < P.p ? 2 : 1;
+        else if (tb == k) b = u < P.p ? k - 1 : k;
+        else if (u < P.p) b = tb - 1;
+        else if (u >= P.one_minus_p) b = tb + 1;
+        else b = tb;
+      } else if (P.err_kind == 2) {  // Confusion, binning.hpp:247-257
+        const double u = P.u_err[idx];
+        const double* row = P.conf + (uint64_t)(tb - 1) * k;
+        double cum = 0.0;
+        b = k;
+        for (uint32_t q = 0; q < k; ++q) {
+          cum = __dadd_rn(cum, row[q]);
+          if (u < cum) {
+            b = q + 1;
+            break;
+          }
+        }
+      } else {
+        b = tb;
+      }
+      if (P.tb_out) P.tb_out[idx] = (uint8_t)tb;
+    }
+    pb[j] = b;
+  }
+  if (flags) atomicOr(&s_flags, flags);
+
+  // stable rank within the warp's 256 consecutive requests: one ballot per bin
+  uint32_t wc = 0;  // lane b: running count of bin b+1 in this warp
+#pragma unroll
+  for (int j = 0; j < IPT; ++j) {
+    uint32_t mine = 0, own = 0;
+    for (uint32_t b = 1; b <= k; ++b) {
+      const uint32_t bal = __ballot_sync(0xffffffffu, pb[j] == b);
+      if (pb[j] == b) mine = bal;
+      if (lane == b - 1) own = bal;
+    }
+    const uint32_t basec = __shfl_sync(0xffffffffu, wc, pb[j] ? pb[j] - 1 : 0);
+    rl[j] = basec + __popc(mine & lanemask_lt());
+    wc += __popc(own);
+  }
+  if (lane < k) s_wcnt[w][lane] = wc;
+  __syncthreads();
+  if (tid == 0 && s_flags) atomicOr(P.ws.flags, s_flags);
+
+  if (w == 0) {
+    uint32_t excl = 0, tot = 0, nfrag = 0;
+    if (lane < k) {
+      uint32_t run = 0;
+      for (int w2 = 0; w2 < NW; ++w2) {
+        s_woff[w2][lane] = run;
+        run += s_wcnt[w2][lane];
+      }
+      tot = run;
+      s_tot[lane] = tot;
+      // phase-1 decoupled look-back on the per-bin counts
+      unsigned long long* d = P.ws.desc1 + (uint64_t)t * k + lane;
+      if (t == 0) {
+        st_release64(d, FLAG_P | tot);
+      } else {
+        st_release64(d, FLAG_A | tot);
+        unsigned long long acc = 0;
+        int64_t p = (int64_t)t - 1;
+        while (true) {
+          unsigned long long v;
+          do {
+            v = ld_acquire64(P.ws.desc1 + (uint64_t)p * k + lane);
+          } while ((v >> 62) == 0);
+          acc += v & VAL_MASK;
+          if ((v >> 62) == 2) break;
+          --p;
+        }
+        excl = (uint32_t)acc;
+        st_release64(d, FLAG_P | (acc + tot));
+      }
+      const uint32_t jlo = P.divB.div(excl);
+      nfrag = tot ? P.divB.div(excl + tot - 1) - jlo + 1 : 0;
+      s_excl[lane] = excl;
+      s_jlo[lane] = jlo;
+      s_nfrag[lane] = nfrag;
+    }
+    uint32_t incl = nfrag;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    if (lane < k) s_fbase[lane] = incl - nfrag;
+    if (lane == 31) s_nfrag_total = incl;
+    // closings before this tile = sum_b floor(excl_b / B)
+    uint32_t cb = lane < k ? P.divB.div(excl) : 0;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) cb += __shfl_xor_sync(0xffffffffu, cb, o);
+    if (lane == 0) s_closebase = cb;
+  }
+  __syncthreads();
+  for (uint32_t i = tid; i < s_nfrag_total; i += TB) s_slot[i] = 0ull;
+  __syncthreads();
+
+  uint32_t rk[IPT], jb[IPT];
+#pragma unroll
+  for (int j = 0; j < IPT; ++j) {
+    rk[j] = 0;
+    jb[j] = 0;
+    if (pb[j]) {
+      const uint32_t b = pb[j] - 1;
+      rk[j] = s_excl[b] + s_woff[w][b] + rl[j];
+      jb[j] = P.divB.div(rk[j]);
+      atomicMax(&s_slot[s_fbase[b] + (jb[j] - s_jlo[b])],
+                (unsigned long long)__double_as_longlong(sv[j]));
+    }
+  }
+  __syncthreads();
+
+  // phase-2 look-back: the open batch's running max carried across tiles.
+  // Tile transform for bin b: f(x) = alpha ? max(x, c) : c.
+  if (w == 0 && lane < k) {
+    const uint32_t excl = s_excl[lane], tot = s_tot[lane];
+    uint32_t alpha;
+    unsigned long long c;
+    if (tot == 0) {
+      alpha = 1;
+      c = 0;
+    } else {
+      const uint32_t jin = s_jlo[lane], end = excl + tot, jout = P.divB.div(end);
+      if (jout == jin) {
+        alpha = 1;
+        c = s_slot[s_fbase[lane]];
+      } else {
+        alpha = 0;
+        c = (end - jout * B) ? s_slot[s_fbase[lane] + s_nfrag[lane] - 1] : 0ull;
+      }
+    }
+    unsigned long long* dv = P.ws.desc2v + (uint64_t)t * k + lane;
+    uint32_t* df = P.ws.desc2f + (uint64_t)t * k + lane;
+    unsigned long long xin = 0, inclv;
+    if (t == 0) {
+      inclv = c;
+      *dv = inclv;
+      __threadfence();
+      st_release32(df, 2);
+    } else {
+      *dv = ((unsigned long long)alpha << 63) | c;
+      __threadfence();
+      st_release32(df, 1);
+      unsigned long long gc = 0;
+      int64_t p = (int64_t)t - 1;
+      while (true) {
+        uint32_t f;
+        do {
+          f = ld_acquire32(P.ws.desc2f + (uint64_t)p * k + lane);
+        } while (f == 0);
+        const unsigned long long v = ld_relaxed64(P.ws.desc2v + (uint64_t)p * k + lane);
+        if (f == 2) {
+          xin = v > gc ? v : gc;
+          break;
+        }
+        const unsigned long long cp = v & ~(1ull << 63);
+        gc = cp > gc ? cp : gc;
+        if (!(v >> 63)) {
+          xin = gc;
+          break;
+        }
+        --p;
+      }
+      inclv = alpha ? (xin > c ? xin : c) : c;
+      *dv = inclv;
+      __threadfence();
+      st_release32(df, 2);
+    }
+    if (tot) {
+      unsigned long long* s0 = &s_slot[s_fbase[lane]];
+      if (xin > *s0) *s0 = xin;
+    }
+    if (t == P.ntiles - 1) {
+      P.ws.fin_cnt[lane] = (unsigned long long)excl + tot;
+      P.ws.fin_open[lane] = inclv;
+    }
+  }
+  __syncthreads();
+
+  // closing records, in closing-request order (dispatch order on the fast path)
+  uint32_t wtot = 0;
+  bool closing[IPT];
+#pragma unroll
+  for (int j = 0; j < IPT; ++j) {
+    closing[j] = pb[j] && (rk[j] - jb[j] * B == B - 1);
+    wtot += __popc(__ballot_sync(0xffffffffu, closing[j]));
+  }
+  if (lane == 0) s_wclose[w] = wtot;
+  __syncthreads();
+  uint32_t run = s_closebase;
+  for (uint32_t w2 = 0; w2 < w; ++w2) run += s_wclose[w2];
+#pragma unroll
+  for (int j = 0; j < IPT; ++j) {
+    const uint64_t idx = wbase + j * 32 + lane;
+    const uint32_t bal = __ballot_sync(0xffffffffu, closing[j]);
+    if (closing[j]) {
+      const uint32_t q = run + __popc(bal & lanemask_lt());
+      const uint32_t b = pb[j] - 1;
+      P.ws.recR[q] = av[j];
+      P.ws.recS[q] = __longlong_as_double((long long)s_slot[s_fbase[b] + (jb[j] - s_jlo[b])]);
+      P.ws.recBin[q] = (uint8_t)pb[j];
+      P.ws.recJ[q] = jb[j];
+      P.ws.recC[q] = (uint32_t)idx;
+    }
+    run += __popc(bal);
+    if (idx < n) {
+      P.ws.pb8[idx] = (uint8_t)pb[j];
+      P.ws.rank[idx] = rk[j];
+    }
+  }
+}
+
+// Drain partials, batch counts, dispatch-order bases (one warp).
+__global__ void finalize_kernel(WS ws, const double* a, uint32_t n, uint32_t k, uint32_t B,
+                                int32_t flush) {
+  const uint32_t lane = threadIdx.x;
+  Info* I = ws.info;
+  const uint32_t fl = *ws.flags;
+  uint32_t F = 0, rem = 0, part = 0;
+  if (lane < k) {
+    const uint32_t cnt = (uint32_t)ws.fin_cnt[lane];
+    F = cnt / B;
+    rem = cnt - F * B;
+    part = flush && rem > 0;
+  }
+  auto scan = [&](uint32_t v) {
+    uint32_t x = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    return x;  // inclusive
+  };
+  const uint32_t nbat = F + part;
+  const uint32_t ib = scan(nbat), iF = scan(F), ip = scan(part), iz = scan(F >= 1 ? 1u : 0u);
+  const uint32_t dcount = (F ? F - 1 : 0) + part;
+  const uint32_t id = scan(dcount);
+  const uint32_t prem = part ? rem : 0;
+  const uint32_t ipr = scan(prem);
+  const uint32_t nclose = __shfl_sync(0xffffffffu, iF, 31);
+  const uint32_t npart = __shfl_sync(0xffffffffu, ip, 31);
+  const uint32_t Z = __shfl_sync(0xffffffffu, iz, 31);
+  // requests before bin b's drain batches (overload + flush)
+  unsigned long long dr = (unsigned long long)B * (F ? F - 1 : 0) + prem, idr = dr;
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long y = __shfl_up_sync(0xffffffffu, idr, o);
+    if (lane >= o) idr += y;
+  }
+  if (lane < k) {
+    I->F[lane] = F;
+    I->rem[lane] = rem;
+    I->nbat[lane] = nbat;
+    I->bin_base[lane] = ib - nbat;
+    I->dbase[lane] = id - dcount;
+    I->dreq[lane] = (unsigned long long)B * Z + (idr - dr);
+    I->pfirst[lane] = nclose * B + (ipr - prem);
+    I->cfirst[lane] = 0xFFFFFFFFu;
+    if (part) {  // on_drain partial: formed at the last arrival (simulator.hpp:203-205,220)
+      const uint32_t q = nclose + (ip - part);
+      ws.recR[q] = a[n - 1];
+      ws.recS[q] = __longlong_as_double((long long)ws.fin_open[lane]);
+      ws.recBin[q] = (uint8_t)(lane + 1);
+      ws.recJ[q] = F;
+      ws.recC[q] = 0xFFFFFFFFu;
+    }
+  }
+  unsigned long long ncl = lane < k ? (unsigned long long)F * B + (flush ? rem : 0) : 0;
+  for (int o = 16; o; o >>= 1) ncl += __shfl_xor_sync(0xffffffffu, ncl, o);
+  if (lane == 0) {
+    I->nclose = nclose;
+    I->npartial = npart;
+    I->nb = nclose + npart;
+    I->Z = Z;
+    I->nc = ncl;
+    I->flags = fl;
+    I->path = (fl & FL_NONMONO) ? 3 : !(fl & FL_NOT_ALL_EQUAL) ? 1 : (fl & FL_TIE_GT_B) ? 2 : 0;
+  }
+}
+
+// Overload: closing index of each bin's first batch (round-0 order key).
+__global__ void ovl_first_kernel(WS ws, uint32_t nclose) {
+  const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < nclose && ws.recJ[q] == 0) ws.info->cfirst[ws.recBin[q] - 1] = ws.recC[q];
+}
+
+// Dispatch position of every record + map (bin, j) -> position + member offset.
+// path 0: closing order, partials after (App. A.2 strictly increasing arrivals)
+// path 1: one tie group (overload): rounds in first-closing order, drains.
+__global__ void order_kernel(WS ws, uint32_t* map, uint32_t* order, uint32_t* dfirst,
+                             uint32_t k, uint32_t B, int32_t flush, int32_t path) {
+  const Info* I = ws.info;
+  const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= I->nb) return;
+  const uint32_t b = ws.recBin[q] - 1, j = ws.recJ[q];
+  const bool partial = q >= I->nclose;
+  uint32_t pos;
+  unsigned long long before;
+  if (path == 0) {
+    pos = q;
+    before = partial ? I->pfirst[b] : (unsigned long long)q * B;
+  } else {
+    const uint32_t Fb = I->F[b];
+    if (partial) {
+      pos = I->Z + I->dbase[b] + (Fb ? Fb - 1 : 0);
+      before = I->dreq[b] + (unsigned long long)B * (Fb ? Fb - 1 : 0);
+    } else if (flush && j >= 1) {
+      pos = I->Z + I->dbase[b] + (j - 1);
+      before = I->dreq[b] + (unsigned long long)B * (j - 1);
+    } else {
+      const uint32_t cb = I->cfirst[b];
+      uint32_t p = 0;
+      for (uint32_t q2 = 0; q2 < k; ++q2) {
+        const uint32_t F = I->F[q2];
+        if (!flush) p += F < j ? F : j;
+        p += (I->cfirst[q2] < cb) && (F > j);
+      }
+      pos = p;
+      before = (unsigned long long)B * p;
+    }
+  }
+  order[pos] = q;
+  map[I->bin_base[b] + j] = pos;
+  dfirst[pos] = (uint32_t)before;
+}
+
+__global__ void gather_kernel(WS ws, const uint32_t* order, int32_t path, uint32_t B, double* dR,
+                              double* dS, uint8_t* dBin, uint32_t* dSize) {
+  const Info* I = ws.info;
+  const uint32_t d = blockIdx.x * blockDim.x + threadIdx.x;
+  if (d >= I->nb) return;
+  const uint32_t q = path == 0 ? d : order[d];
+  dR[d] = ws.recR[q];
+  dS[d] = ws.recS[q];
+  const uint8_t b = ws.recBin[q];
+  if (dBin) dBin[d] = b;
+  if (dSize) dSize[d] = q < I->nclose ? B : I->rem[b - 1];
+}
+
+// ---------------------------------------------------------------- Lindley
+struct LArgs {
+  const double* R;
+  const double* S;
+  uint32_t nb;
+  uint8_t* split;
+  double* busy_part;
+  double *aggA, *aggC, *incA, *incC;
+  uint32_t* flag;
+  uint32_t* counter;
+  double tol_rel;
+};
+
+struct MP {  // f(x) = max(x + A, C)
+  double A, C;
+};
+__device__ __forceinline__ MP compose(const MP& f, const MP& g) {  // g after f
+  return MP{f.A + g.A, fmax(f.C + g.A, g.C)};
+}
+
+__global__ void __launch_bounds__(LB) lindley_scan_kernel(LArgs L) {
+  __shared__ MP s_w[LB / 32];
+  __shared__ MP s_prefix;
+  __shared__ double s_busy[LB / 32];
+  __shared__ uint32_t s_blk;
+  const uint32_t tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  if (tid == 0) s_blk = atomicAdd(L.counter, 1u);
+  __syncthreads();
+  const uint32_t blk = s_blk;
+  const uint64_t d0 = (uint64_t)blk * LTILE + tid * LI;
+  double R[LI], S[LI];
+  MP f{0.0, -CUDART_INF};
+  double bs = 0.0;
+#pragma unroll
+  for (int i = 0; i < LI; ++i) {
+    const bool v = d0 + i < L.nb;
+    R[i] = v ? L.R[d0 + i] : -CUDART_INF;
+    S[i] = v ? L.S[d0 + i] : 0.0;
+    f = compose(f, MP{S[i], R[i] + S[i]});
+    bs += S[i];
+  }
+  // inclusive scan over the block's threads
+  MP x = f;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    MP y;
+    y.A = __shfl_up_sync(0xffffffffu, x.A, o);
+    y.C = __shfl_up_sync(0xffffffffu, x.C, o);
+    if (lane >= o) x = compose(y, x);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) bs += __shfl_xor_sync(0xffffffffu, bs, o);
+  if (lane == 31) s_w[w] = x;
+  if (lane == 0) s_busy[w] = bs;
+  __syncthreads();
+  if (w == 0) {
+    MP agg{0.0, -CUDART_INF};
+    for (int w2 = 0; w2 < LB / 32; ++w2) agg = compose(agg, s_w[w2]);
+    if (lane == 0) {
+      double b2 = 0.0;
+      for (int w2 = 0; w2 < LB / 32; ++w2) b2 += s_busy[w2];
+      L.busy_part[blk] = b2;
+      MP pre{0.0, -CUDART_INF};
+      if (blk == 0) {
+        L.incA[0] = agg.A;
+        L.incC[0] = agg.C;
+        __threadfence();
+        st_release32(&L.flag[0], 2);
+      } else {
+        L.aggA[blk] = agg.A;
+        L.aggC[blk] = agg.C;
+        __threadfence();
+        st_release32(&L.flag[blk], 1);
+        MP acc{0.0, -CUDART_INF};  // composition of visited predecessors (later ones first)
+        int64_t p = (int64_t)blk - 1;
+        while (true) {
+          uint32_t fl;
+          do {
+            fl = ld_acquire32(&L.flag[p]);
+          } while (fl == 0);
+          MP v;
+          if (fl == 2) {
+            v.A = *(volatile double*)&L.incA[p];
+            v.C = *(volatile double*)&L.incC[p];
+            acc = compose(v, acc);
+            break;
+          }
+          v.A = *(volatile double*)&L.aggA[p];
+          v.C = *(volatile double*)&L.aggC[p];
+          acc = compose(v, acc);
+          --p;
+        }
+        pre = acc;
+        const MP inc = compose(pre, agg);
+        L.incA[blk] = inc.A;
+        L.incC[blk] = inc.C;
+        __threadfence();
+        st_release32(&L.flag[blk], 2);
+      }
+      s_prefix = pre;
+    }
+  }
+  __syncthreads();
+  // exclusive prefix of this thread = block prefix, earlier warps, earlier lanes
+  MP pre = s_prefix;
+  for (uint32_t w2 = 0; w2 < w; ++w2) pre = compose(pre, s_w[w2]);
+  MP xl;
+  xl.A = __shfl_up_sync(0xffffffffu, x.A, 1);
+  xl.C = __shfl_up_sync(0xffffffffu, x.C, 1);
+  if (lane > 0) pre = compose(pre, xl);
+  double Dp = pre.C;  // applied to D_{-1} = -inf (server idle before the first batch)
+#pragma unroll
+  for (int i = 0; i < LI; ++i) {
+    if (d0 + i < L.nb) {
+      bool sp;
+      if (Dp == -CUDART_INF) sp = true;
+      else sp = R[i] > Dp + L.tol_rel * fmax(fabs(Dp), fabs(R[i]));
+      L.split[d0 + i] = sp;
+      Dp = fmax(Dp, R[i]) + S[i];
+    }
+  }
+}
+
+// Exact serial recurrence inside every certified busy period.
+__global__ void lindley_segments_kernel(const double* __restrict__ R, const double* __restrict__ S,
+                                        const uint8_t* __restrict__ split, uint32_t nb,
+                                        double* __restrict__ start, double* __restrict__ finish) {
+  const uint32_t d = blockIdx.x * blockDim.x + threadIdx.x;
+  if (d >= nb || !split[d]) return;
+  double D = __dadd_rn(R[d], S[d]);  // idle server: start = formation time
+  start[d] = R[d];
+  finish[d] = D;
+  constexpr int CH = 16;
+  for (uint32_t e0 = d + 1; e0 < nb; e0 += CH) {
+    double r[CH], s[CH];
+    uint8_t sp[CH];
+#pragma unroll
+    for (int i = 0; i < CH; ++i) {
+      const bool v = e0 + i < nb;
+      sp[i] = v ? split[e0 + i] : 1;
+      r[i] = v ? R[e0 + i] : 0.0;
+      s[i] = v ? S[e0 + i] : 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < CH; ++i) {
+      if (sp[i]) return;
+      const double st = fmax(D, r[i]);
+      D = __dadd_rn(st, s[i]);
+      start[e0 + i] = st;
+      finish[e0 + i] = D;
+    }
+  }
+}
+
+// ------------------------------------------------------------- requests
+struct QArgs {
+  const double* a;
+  const uint8_t* pb8;
+  const uint32_t* rank;
+  const uint32_t* map;
+  const double* finish;
+  const uint32_t* dfirst;
+  const Info* info;
+  FastDiv divB;
+  uint32_t n, B;
+  unsigned long long* key;
+  double* lat_part;
+  unsigned long long* kminmax;
+  double* completion;
+  uint32_t* batch;
+  uint32_t* members;
+};
+
+__global__ void __launch_bounds__(256) request_kernel(QArgs Q) {
+  __shared__ double s_sum[8];
+  __shared__ unsigned long long s_min[8], s_max[8];
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double lat = 0.0;
+  unsigned long long kmin = KEY_UNSERVED, kmax = 0;
+  if (i < Q.n) {
+    const uint32_t b = Q.pb8[i];
+    unsigned long long key = KEY_UNSERVED;
+    double comp = CUDART_NAN;
+    uint32_t bid = BB_NO_BATCH;
+    if (b) {
+      const uint32_t r = Q.rank[i];
+      const uint32_t j = Q.divB.div(r);
+      if (j < Q.info->nbat[b - 1]) {
+        const uint32_t d = Q.map[Q.info->bin_base[b - 1] + j];
+        comp = Q.finish[d];
+        lat = __dsub_rn(comp, Q.a[i]);  // simulator.hpp:294
+        key = (unsigned long long)__double_as_longlong(lat);
+        kmin = kmax = key;
+        bid = d;
+        if (Q.members) Q.members[Q.dfirst[d] + (r - j * Q.B)] = i;
+      }
+    }
+    Q.key[i] = key;
+    if (Q.completion) Q.completion[i] = comp;
+    if (Q.batch) Q.batch[i] = bid;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    lat += __shfl_xor_sync(0xffffffffu, lat, o);
+    const unsigned long long a = __shfl_xor_sync(0xffffffffu, kmin, o);
+    const unsigned long long b = __shfl_xor_sync(0xffffffffu, kmax, o);
+    kmin = a < kmin ? a : kmin;
+    kmax = b > kmax ? b : kmax;
+  }
+  if (lane == 0) {
+    s_sum[w] = lat;
+    s_min[w] = kmin;
+    s_max[w] = kmax;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int q = 0; q < 8; ++q) {
+      s += s_sum[q];
+      kmin = s_min[q] < kmin ? s_min[q] : kmin;
+      kmax = s_max[q] > kmax ? s_max[q] : kmax;
+    }
+    Q.lat_part[blockIdx.x] = s;
+    if (kmin != KEY_UNSERVED) {
+      atomicMin(&Q.kminmax[0], kmin);
+      atomicMax(&Q.kminmax[1], kmax);
+    }
+  }
+}
+
+// deterministic sum of block partials (one block)
+__global__ void sum_kernel(const double* part, uint32_t m, double* out) {
+  __shared__ double s[256];
+  double acc = 0.0;
+  for (uint32_t i = threadIdx.x; i < m; i += 256) acc += part[i];
+  s[threadIdx.x] = acc;
+  __syncthreads();
+  for (int o = 128; o; o >>= 1) {
+    if (threadIdx.x < o) s[threadIdx.x] += s[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = s[0];
+}
+
+// --------------------------------------------------------------- selection
+__global__ void hist_kernel(const unsigned long long* __restrict__ key, uint32_t m,
+                            unsigned long long lo, unsigned long long hi, uint32_t shift,
+                            uint32_t* __restrict__ hist) {
+  __shared__ uint32_t h[HBINS];
+  for (int i = threadIdx.x; i < HBINS; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+    const unsigned long long v = key[i];
+    if (v >= lo && v <= hi) atomicAdd(&h[(uint32_t)((v - lo) >> shift)], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < HBINS; i += blockDim.x)
+    if (h[i]) atomicAdd(&hist[i], h[i]);
+}
+
+__global__ void collect_kernel(const unsigned long long* __restrict__ key, uint32_t m,
+                               unsigned long long lo, unsigned long long hi,
+                               unsigned long long* __restrict__ out, uint32_t* __restrict__ count) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+    const unsigned long long v = key[i];
+    if (v >= lo && v <= hi) out[atomicAdd(count, 1u)] = v;
+  }
+}
+
+// ------------------------------------------------------------------ host
+#define BB_CK(x)                                                                        \
+  do {                                                                                  \
+    cudaError_t e_ = (x);                                                               \
+    if (e_ != cudaSuccess) {                                                            \
+      R->status = BB_ECUDA;                                                             \
+      snprintf(R->message, sizeof R->message, "CUDA error %s at %s:%d",                 \
+               cudaGetErrorString(e_), __FILE__, __LINE__);                             \
+      goto cleanup;                                                                     \
+    }                                                                                   \
+  } while (0)
+
+struct Pool {
+  std::vector<void*> ptrs;
+  cudaStream_t s;
+  cudaError_t alloc(void** p, size_t bytes) {
+    cudaError_t e = cudaMallocAsync(p, bytes ? bytes : 8, s);
+    if (e == cudaSuccess) ptrs.push_back(*p);
+    return e;
+  }
+  ~Pool() {
+    for (void* p : ptrs) cudaFreeAsync(p, s);
+  }
+};
+
+unsigned grid_for(uint64_t n, unsigned t) { return (unsigned)((n + t - 1) / t); }
+
+}  // namespace
+
+// Select the exact order statistics of `rank`s among keys (all keys of
+// completed requests lie in [kmin, kmax]; unserved keys are above).
+static cudaError_t select_ranks(const unsigned long long* keys, uint32_t n,
+                                unsigned long long kmin, unsigned long long kmax,
+                                const std::vector<unsigned long long>& ranks,
+                                std::vector<unsigned long long>& vals, Pool& pool,
+                                cudaStream_t s) {
+  vals.assign(ranks.size(), kmin);
+  if (kmin == kmax) return cudaSuccess;
+  uint32_t* d_hist = nullptr;
+  uint32_t* d_cnt = nullptr;
+  unsigned long long *bufA = nullptr, *bufB = nullptr;
+  cudaError_t e;
+  if ((e = pool.alloc((void**)&d_hist, HBINS * sizeof(uint32_t)))) return e;
+  if ((e = pool.alloc((void**)&d_cnt, sizeof(uint32_t)))) return e;
+  std::vector<uint32_t> h(HBINS);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const unsigned grid = (unsigned)sms * 4;
+  for (size_t t = 0; t < ranks.size(); ++t) {
+    unsigned long long lo = kmin, hi = kmax, rank = ranks[t];
+    const unsigned long long* buf = keys;
+    uint32_t m = n;
+    while (lo < hi) {
+      const unsigned long long span = hi - lo;
+      const int bits = 64 - __builtin_clzll(span);
+      const uint32_t shift = bits > HBITS ? (uint32_t)(bits - HBITS) : 0u;
+      if ((e = cudaMemsetAsync(d_hist, 0, HBINS * sizeof(uint32_t), s))) return e;
+      hist_kernel<<<grid, 256, 0, s>>>(buf, m, lo, hi, shift, d_hist);
+      note_launch();
+      if ((e = cudaMemcpyAsync(h.data(), d_hist, HBINS * sizeof(uint32_t), cudaMemcpyDeviceToHost, s))) return e;
+      if ((e = cudaStreamSynchronize(s))) return e;
+      unsigned long long acc = 0;
+      uint32_t bk = 0;
+      for (; bk < HBINS; ++bk) {
+        if (acc + h[bk] > rank) break;
+        acc += h[bk];
+      }
+      if (bk == HBINS) return cudaErrorUnknown;  // rank beyond the population
+      rank -= acc;
+      const unsigned long long nlo = lo + ((unsigned long long)bk << shift);
+      unsigned long long nhi = nlo + ((1ull << shift) - 1);
+      if (nhi > hi || nhi < nlo) nhi = hi;
+      lo = nlo;
+      hi = nhi;
+      if (lo == hi) break;
+      // compact the bucket's members for the next level (sizes only shrink)
+      unsigned long long* dst;
+      if (buf == keys) {
+        if ((e = pool.alloc((void**)&bufA, (size_t)h[bk] * 8))) return e;
+        if ((e = pool.alloc((void**)&bufB, (size_t)h[bk] * 8))) return e;
+        dst = bufA;
+      } else {
+        dst = buf == bufA ? bufB : bufA;
+      }
+      if ((e = cudaMemsetAsync(d_cnt, 0, sizeof(uint32_t), s))) return e;
+      collect_kernel<<<grid, 256, 0, s>>>(buf, m, lo, hi, dst, d_cnt);
+      note_launch();
+      buf = dst;
+      m = h[bk];
+    }
+    vals[t] = lo;
+  }
+  return cudaSuccess;
+}
+
+void trace_run(const TraceArgs& A, TraceResult* R, cudaStream_t s) {
+  std::memset(R, 0, sizeof *R);
+  R->status = BB_OK;
+  R->k = A.k;
+  Pool pool;
+  pool.s = s;
+  const uint32_t n = A.n, k = A.k, B = A.B;
+  const uint32_t ntiles = (n + TILE - 1) / TILE;
+  const uint64_t rec_cap = (uint64_t)n / B + k + 1;
+  WS ws{};
+  Info info{};
+  DevError herr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr;
+  double *dR = nullptr, *dS = nullptr, *start = nullptr, *finish = nullptr;
+  uint32_t *map = nullptr, *order = nullptr, *dfirst = nullptr, *dsize = nullptr;
+  uint8_t *dbin = nullptr, *split = nullptr;
+  BB_CK(cudaEventCreate(&ev0));
+  BB_CK(cudaEventCreate(&ev1));
+  BB_CK(cudaEventCreate(&ev2));
+  BB_CK(pool.alloc((void**)&ws.counters, 16));
+  BB_CK(pool.alloc((void**)&ws.desc1, (size_t)ntiles * k * 8));
+  BB_CK(pool.alloc((void**)&ws.desc2v, (size_t)ntiles * k * 8));
+  BB_CK(pool.alloc((void**)&ws.desc2f, (size_t)ntiles * k * 4));
+  BB_CK(pool.alloc((void**)&ws.pb8, n));
+  BB_CK(pool.alloc((void**)&ws.rank, (size_t)n * 4));
+  BB_CK(pool.alloc((void**)&ws.recR, rec_cap * 8));
+  BB_CK(pool.alloc((void**)&ws.recS, rec_cap * 8));
+  BB_CK(pool.alloc((void**)&ws.recBin, rec_cap));
+  BB_CK(pool.alloc((void**)&ws.recJ, rec_cap * 4));
+  BB_CK(pool.alloc((void**)&ws.recC, rec_cap * 4));
+  BB_CK(pool.alloc((void**)&ws.fin_cnt, 32 * 8));
+  BB_CK(pool.alloc((void**)&ws.fin_open, 32 * 8));
+  BB_CK(pool.alloc((void**)&ws.flags, 4));
+  BB_CK(pool.alloc((void**)&ws.err, sizeof(DevError)));
+  BB_CK(pool.alloc((void**)&ws.info, sizeof(Info)));
+  BB_CK(cudaMemsetAsync(ws.counters, 0, 16, s));
+  BB_CK(cudaMemsetAsync(ws.desc1, 0, (size_t)ntiles * k * 8, s));
+  BB_CK(cudaMemsetAsync(ws.desc2f, 0, (size_t)ntiles * k * 4, s));
+  BB_CK(cudaMemsetAsync(ws.fin_cnt, 0, 32 * 8, s));
+  BB_CK(cudaMemsetAsync(ws.fin_open, 0, 32 * 8, s));
+  BB_CK(cudaMemsetAsync(ws.flags, 0, 4, s));
+  BB_CK(cudaMemsetAsync(ws.err, 0xFF, 8, s));
+  BB_CK(cudaEventRecord(ev0, s));
+  {
+    PartArgs P{};
+    P.a = A.a;
+    P.s = A.s;
+    P.u_err = A.u_err;
+    P.pred = A.pred;
+    P.edges = A.edges;
+    P.conf = A.conf;
+    P.tb_out = A.req_true_bin;
+    P.n = n;
+    P.B = B;
+    P.k = k;
+    P.ntiles = ntiles;
+    P.err_kind = A.err_kind;
+    P.p = A.p_error;
+    P.one_minus_p = 1.0 - A.p_error;
+    P.divB = FastDiv(B);
+    P.ws = ws;
+    partition_kernel<<<ntiles, TB, 0, s>>>(P);
+    note_launch();
+    BB_CK(cudaGetLastError());
+  }
+  BB_CK(cudaEventRecord(ev1, s));
+  if (A.req_pred_bin) BB_CK(cudaMemcpyAsync(A.req_pred_bin, ws.pb8, n, cudaMemcpyDeviceToDevice, s));
+  finalize_kernel<<<1, 32, 0, s>>>(ws, A.a, n, k, B, A.flush);
+  note_launch();
+  BB_CK(cudaGetLastError());
+  BB_CK(cudaMemcpyAsync(&info, ws.info, sizeof(Info), cudaMemcpyDeviceToHost, s));
+  BB_CK(cudaMemcpyAsync(&herr, ws.err, sizeof(DevError), cudaMemcpyDeviceToHost, s));
+  BB_CK(cudaStreamSynchronize(s));
+  if (herr.packed != ~0ull) {
+    const unsigned long long idx = herr.packed >> 8;
+    const int code = (int)(herr.packed & 0xFF);
+    R->status = code;
+    if (code == BB_EDOMAIN && herr.aux == 1)
+      snprintf(R->message, sizeof R->message, "simulation: drew a non-positive service time");
+    else if (code == BB_EDOMAIN)
+      snprintf(R->message, sizeof R->message, "assign_bin: length %.17g outside bin support",
+               herr.value);
+    else
+      snprintf(R->message, sizeof R->message, "request %llu: predicted bin %g out of range", idx,
+               herr.value);
+    goto cleanup;
+  }
+  if (info.path == 3) {
+    R->status = BB_EINVAL;
+    snprintf(R->message, sizeof R->message, "trace arrays: arrivals must be non-decreasing");
+    goto cleanup;
+  }
+  if (info.path == 2) {
+    R->status = BB_EUNSUPPORTED;
+    snprintf(R->message, sizeof R->message,
+             "trace arrays: a tie group of more than B equal arrivals (other than a single "
+             "all-equal group) is not supported yet");
+    goto cleanup;
+  }
+  R->path = (int32_t)info.path;
+  {
+    const uint32_t nb = info.nb;
+    R->n_batches = nb;
+    R->n_completed = info.nc;
+    for (uint32_t b = 0; b < k; ++b) R->per_bin[b] = info.nbat[b];
+    if (nb == 0) goto cleanup;  // nothing served: metrics stay zero (finish(), :283)
+    BB_CK(pool.alloc((void**)&map, (size_t)nb * 4));
+    BB_CK(pool.alloc((void**)&order, (size_t)nb * 4));
+    BB_CK(pool.alloc((void**)&dfirst, (size_t)nb * 4));
+    BB_CK(pool.alloc((void**)&dR, (size_t)nb * 8));
+    BB_CK(pool.alloc((void**)&dS, (size_t)nb * 8));
+    BB_CK(pool.alloc((void**)&split, nb));
+    start = A.bat_start;
+    finish = A.bat_finish;
+    if (!start) BB_CK(pool.alloc((void**)&start, (size_t)nb * 8));
+    if (!finish) BB_CK(pool.alloc((void**)&finish, (size_t)nb * 8));
+    if (info.path == 1) {
+      ovl_first_kernel<<<grid_for(info.nclose, 256), 256, 0, s>>>(ws, info.nclose);
+      note_launch();
+      BB_CK(cudaGetLastError());
+    }
+    order_kernel<<<grid_for(nb, 256), 256, 0, s>>>(ws, map, order, dfirst, k, B, A.flush,
+                                                   (int32_t)info.path);
+    note_launch();
+    BB_CK(cudaGetLastError());
+    gather_kernel<<<grid_for(nb, 256), 256, 0, s>>>(ws, order, (int32_t)info.path, B, dR, dS,
+                                                    A.bat_bin, A.bat_size);
+    note_launch();
+    BB_CK(cudaGetLastError());
+    // Lindley: certified busy-period splits, then exact serial segments
+    const uint32_t lt = (nb + LTILE - 1) / LTILE;
+    double *aggA, *aggC, *incA, *incC, *busy_part, *busy_sum;
+    uint32_t* lflag;
+    BB_CK(pool.alloc((void**)&aggA, (size_t)lt * 8));
+    BB_CK(pool.alloc((void**)&aggC, (size_t)lt * 8));
+    BB_CK(pool.alloc((void**)&incA, (size_t)lt * 8));
+    BB_CK(pool.alloc((void**)&incC, (size_t)lt * 8));
+    BB_CK(pool.alloc((void**)&busy_part, (size_t)lt * 8));
+    BB_CK(pool.alloc((void**)&busy_sum, 8));
+    BB_CK(pool.alloc((void**)&lflag, (size_t)lt * 4));
+    BB_CK(cudaMemsetAsync(lflag, 0, (size_t)lt * 4, s));
+    {
+      LArgs L{dR, dS, nb, split, busy_part, aggA, aggC, incA, incC, lflag, ws.counters + 1,
+              (double)(nb + 4096) * 0x1.0p-50};
+      lindley_scan_kernel<<<lt, LB, 0, s>>>(L);
+      note_launch();
+      BB_CK(cudaGetLastError());
+    }
+    lindley_segments_kernel<<<grid_for(nb, 128), 128, 0, s>>>(dR, dS, split, nb, start, finish);
+    note_launch();
+    BB_CK(cudaGetLastError());
+    sum_kernel<<<1, 256, 0, s>>>(busy_part, lt, busy_sum);
+    note_launch();
+    BB_CK(cudaGetLastError());
+    // per-request pass
+    unsigned long long *keys, *kminmax;
+    double *lat_part, *lat_sum;
+    const uint32_t qb = grid_for(n, 256);
+    BB_CK(pool.alloc((void**)&keys, (size_t)n * 8));
+    BB_CK(pool.alloc((void**)&kminmax, 16));
+    BB_CK(pool.alloc((void**)&lat_part, (size_t)qb * 8));
+    BB_CK(pool.alloc((void**)&lat_sum, 8));
+    {
+      const unsigned long long init[2] = {KEY_UNSERVED, 0ull};
+      BB_CK(cudaMemcpyAsync(kminmax, init, 16, cudaMemcpyHostToDevice, s));
+      QArgs Q{};
+      Q.a = A.a;
+      Q.pb8 = ws.pb8;
+      Q.rank = ws.rank;
+      Q.map = map;
+      Q.finish = finish;
+      Q.dfirst = dfirst;
+      Q.info = ws.info;
+      Q.divB = FastDiv(B);
+      Q.n = n;
+      Q.B = B;
+      Q.key = keys;
+      Q.lat_part = lat_part;
+      Q.kminmax = kminmax;
+      Q.completion = A.req_completion;
+      Q.batch = A.req_batch;
+      Q.members = A.members;
+      request_kernel<<<qb, 256, 0, s>>>(Q);
+      note_launch();
+      BB_CK(cudaGetLastError());
+      sum_kernel<<<1, 256, 0, s>>>(lat_part, qb, lat_sum);
+      note_launch();
+      BB_CK(cudaGetLastError());
+    }
+    BB_CK(cudaEventRecord(ev2, s));
+    // detail copies of the dispatch-ordered batch records
+    if (A.bat_formed) BB_CK(cudaMemcpyAsync(A.bat_formed, dR, (size_t)nb * 8, cudaMemcpyDeviceToDevice, s));
+    if (A.bat_service) BB_CK(cudaMemcpyAsync(A.bat_service, dS, (size_t)nb * 8, cudaMemcpyDeviceToDevice, s));
+    if (A.bat_first) BB_CK(cudaMemcpyAsync(A.bat_first, dfirst, (size_t)nb * 4, cudaMemcpyDeviceToDevice, s));
+    double last = 0, a0 = 0, busy = 0, lsum = 0;
+    unsigned long long mm[2];
+    BB_CK(cudaMemcpyAsync(&last, finish + nb - 1, 8, cudaMemcpyDeviceToHost, s));
+    BB_CK(cudaMemcpyAsync(&a0, A.a, 8, cudaMemcpyDeviceToHost, s));
+    BB_CK(cudaMemcpyAsync(&busy, busy_sum, 8, cudaMemcpyDeviceToHost, s));
+    BB_CK(cudaMemcpyAsync(&lsum, lat_sum, 8, cudaMemcpyDeviceToHost, s));
+    BB_CK(cudaMemcpyAsync(mm, kminmax, 16, cudaMemcpyDeviceToHost, s));
+    BB_CK(cudaStreamSynchronize(s));
+    const unsigned long long nc = info.nc;
+    if (nc > 0) {  // finish(), simulator.hpp:283-301
+      R->makespan = last - a0;
+      R->throughput = (double)nc / R->makespan;
+      R->busy = busy;
+      R->busy_fraction = busy / (1.0 * R->makespan);
+      R->latency_sum = lsum;
+      R->latency_mean = lsum / (double)nc;
+      // interpolated_quantile, binning.hpp:98-104
+      const double qs[2] = {0.50, 0.99};
+      std::vector<unsigned long long> ranks;
+      unsigned long long idxs[2];
+      double fracs[2];
+      for (int q = 0; q < 2; ++q) {
+        const volatile double pos = qs[q] * (double)(nc - 1);
+        idxs[q] = (unsigned long long)pos;
+        fracs[q] = pos - (double)idxs[q];
+        ranks.push_back(idxs[q]);
+        if (idxs[q] + 1 < nc) ranks.push_back(idxs[q] + 1);
+      }
+      std::vector<unsigned long long> vals;
+      BB_CK(select_ranks(keys, n, mm[0], mm[1], ranks, vals, pool, s));
+      size_t vi = 0;
+      double outq[2];
+      for (int q = 0; q < 2; ++q) {
+        double lo, hi;
+        std::memcpy(&lo, &vals[vi++], 8);
+        if (idxs[q] + 1 >= nc) {
+          outq[q] = lo;
+          continue;
+        }
+        std::memcpy(&hi, &vals[vi++], 8);
+        const volatile double diff = hi - lo;
+        const volatile double prod = fracs[q] * diff;
+        outq[q] = lo + prod;
+      }
+      R->p50 = outq[0];
+      R->p99 = outq[1];
+    }
+    float ms = 0;
+    cudaEventElapsedTime(&ms, ev0, ev1);
+    R->ms_partition = ms;
+    cudaEventElapsedTime(&ms, ev0, ev2);
+    R->ms_total = ms;
+  }
+cleanup:
+  if (ev0) cudaEventDestroy(ev0);
+  if (ev1) cudaEventDestroy(ev1);
+  if (ev2) cudaEventDestroy(ev2);
+  (void)dsize;
+  (void)dbin;
+}
+
+}  // namespace bb

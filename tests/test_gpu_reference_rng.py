@@ -1,0 +1,115 @@
+"""run_simulation / replay_trace with the reference's own random streams
+(rng="reference"): the B200 engine reproduces the reference binary's
+SimResult bit-for-bit (scalar sums within the reassociation bound)."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle_py as O
+import paper_2412_04504_b200 as bb
+from _helpers import same_bits, sum_tol
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not O.have_reference(), reason="reference shim not built")]
+
+
+CASES = [
+    dict(arrival_rate=0.95 * 1.385550, n_requests=50000, batch_size=16, k=8, seed=1001,
+         error=("symmetric", 0.1)),
+    dict(arrival_rate=math.inf, n_requests=12800, batch_size=128, k=3, seed=77, flush=False),
+    dict(arrival_rate=math.inf, n_requests=12807, batch_size=128, k=5, seed=78, flush=True,
+         error=("symmetric", 0.25)),
+    dict(arrival_rate=3.0, n_requests=2000, batch_size=8, k=3, seed=11,
+         error=("confusion", [[0.7, 0.25, 0.05], [0.15, 0.7, 0.15], [0.02, 0.28, 0.7]])),
+    dict(arrival_rate=7.0, n_requests=997, batch_size=13, k=3, seed=90210,
+         error=("symmetric", 0.15)),
+]
+
+
+def configs(c):
+    edges = bb.uniform_boundaries(c["k"], 1.0, 20.0).edges
+    em, od = bb.Perfect(), {}
+    if "error" in c:
+        kind, p = c["error"]
+        if kind == "symmetric":
+            em, od = bb.Symmetric(p), dict(error="symmetric", p_error=p)
+        else:
+            em, od = bb.Confusion(p), dict(error="confusion", confusion=p)
+    ours = bb.SimConfig(arrival_rate=c["arrival_rate"], n_requests=c["n_requests"],
+                        batch_size=c["batch_size"], bins=bb.BinConfig(edges), error_model=em,
+                        service=bb.Uniform(1.0, 20.0), seed=c["seed"],
+                        flush_partial=c.get("flush", True), rng="reference")
+    ref = dict(arrival_rate=c["arrival_rate"], n_requests=c["n_requests"],
+               batch_size=c["batch_size"], edges=edges, lo=1.0, hi=20.0, seed=c["seed"],
+               flush_partial=c.get("flush", True), **od)
+    return ours, ref
+
+
+@pytest.mark.parametrize("i", range(len(CASES)))
+def test_run_simulation_detailed_matches_reference_binary(i):
+    ours, ref = configs(CASES[i])
+    mr, dr = O.run(O.reference(), ref)
+    res = bb.run_simulation_detailed(ours)
+    r, b = res.requests, res.batches
+    assert same_bits(r["arrival"], dr["req_arrival"])
+    assert same_bits(r["service"], dr["req_service"])
+    assert same_bits(r["true_bin"], dr["req_true_bin"])
+    assert same_bits(r["predicted_bin"], dr["req_pred_bin"])
+    assert same_bits(r["completion"], dr["req_completion"])
+    assert same_bits(b["finish_time"], dr["bat_finish"])
+    assert same_bits(b["start_time"], dr["bat_start"])
+    assert same_bits(b["formed_time"], dr["bat_formed"])
+    assert same_bits(b["members"], dr["members"])
+    m = res.metrics
+    n = ours.n_requests
+    for key in ("makespan", "throughput", "latency_p50", "latency_p99"):
+        assert same_bits(getattr(m, key), mr[key]), key
+    lat = dr["req_completion"] - dr["req_arrival"]
+    assert abs(m.latency_mean - mr["latency_mean"]) <= sum_tol(n, np.nansum(np.abs(lat))) / mr["n_completed"]
+    # metrics-only entry agrees with the detailed one
+    m2 = bb.run_simulation(ours)
+    assert same_bits(m2.throughput, m.throughput) and same_bits(m2.latency_p99, m.latency_p99)
+
+
+def test_replay_trace_resample_matches_reference():
+    # acceptance.cpp criterion 10 setting (Pareto-like trace, B=32, overload, resample)
+    rs = np.random.default_rng(424242)
+    trace = np.minimum((1.0 - rs.random(20000)) ** (-1.0 / 1.2), 500.0)
+    for k in (1, 4, 16, 32):
+        edges = bb.empirical_boundaries(k, trace).edges
+        seed = bb.replication_seed(1001, 3)
+        ours = bb.SimConfig(arrival_rate=bb.kOverload, n_requests=12800, batch_size=32,
+                            bins=bb.BinConfig(edges), seed=seed, flush_partial=False,
+                            trace_mode="resample", rng="reference")
+        mr, dr = O.run(O.reference(), dict(arrival_rate=math.inf, n_requests=12800, batch_size=32,
+                                           edges=edges, seed=seed, flush_partial=False,
+                                           service="trace_resample", table=trace))
+        m = bb.replay_trace(ours, trace)
+        assert same_bits(m.throughput, mr["throughput"])
+        assert same_bits(m.latency_p50, mr["latency_p50"])
+
+
+def test_run_experiment_reference_streams_bit_exact_throughput():
+    # acceptance criterion 1 protocol (B=128, U[1,20], overload, no flush, 10 seeds)
+    base = bb.RunTemplate(n_requests=12800, batch_size=128, flush_partial=False,
+                          service=bb.ServiceSpec("uniform", 1.0, 20.0))
+    spec = bb.ExperimentSpec(base=base, axes=[bb.SweepAxis("k", [1, 2, 3, 5])], replications=10,
+                             seed=1001, rng="reference")
+    pts = bb.run_experiment(spec)
+    want = {1: 6.447, 2: 8.438, 3: 9.392, 5: 10.34}  # proj/test_output.txt:17
+    for p in pts:
+        assert f"{p.throughput_mean:.4g}" == f"{want[p.k]:.4g}"
+        ref_thr = []
+        for r in range(10):
+            mr, _ = O.run(O.reference(), dict(arrival_rate=math.inf, n_requests=12800,
+                                              batch_size=128,
+                                              edges=bb.uniform_boundaries(p.k, 1.0, 20.0).edges,
+                                              lo=1.0, hi=20.0, seed=bb.replication_seed(1001, r),
+                                              flush_partial=False), detail=False)
+            ref_thr.append(mr["throughput"])
+        mean = 0.0
+        for x in ref_thr:
+            mean += x
+        mean /= 10
+        assert same_bits(p.throughput_mean, mean)
