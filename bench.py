@@ -248,11 +248,14 @@ def main():
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
     results = {}
 
+    from paper_2412_04504_b200 import dist as bbdist
+
+    lo, hi = bbdist.weak_shard(R, rank)
+
     def step():
         rep.zero_()
-        bb.points_shard_device(tpl, Rtot, SEED, rank * R, (rank + 1) * R, rep.data_ptr(), sptr)
-        if world > 1:
-            dist.all_reduce(rep)
+        bb.points_shard_device(tpl, Rtot, SEED, lo, hi, rep.data_ptr(), sptr)
+        bbdist.combine(rep)  # the sweep's one NCCL all-reduce (no-op at N=1)
         results["pts"] = bb.points_reduce_device(tpl, Rtot, rep.data_ptr(), sptr)
 
     for _ in range(args.warmup):

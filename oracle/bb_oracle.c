@@ -100,6 +100,16 @@ void bbo_stream_uniform01(uint64_t seed, uint64_t stream_id, uint64_t n, double*
   free(g);
 }
 
+/* RandomStream(seed).uniform01() n times (rng.hpp:30, :38) -- e.g. the
+ * acceptance suite's trace generator RandomStream trace_rng(424242),
+ * acceptance.cpp:370-374 */
+void bbo_plain_uniform01(uint64_t seed, uint64_t n, double* out) {
+  mt64* g = (mt64*)malloc(sizeof(mt64));
+  stream_init(g, seed);
+  for (uint64_t i = 0; i < n; ++i) out[i] = u01(g);
+  free(g);
+}
+
 /* schedule_arrivals, simulator.hpp:174-185: t += exponential(rate), or t = 0
  * for the overload rate; exponential = -log1p(-u)/rate (rng.hpp:43). */
 void bbo_generate_arrivals(uint64_t seed, double rate, uint64_t n, double* out) {

@@ -116,6 +116,8 @@ uint64_t bbo_splitmix64(uint64_t x);
 uint64_t bbo_replication_seed(uint64_t master, uint64_t rep);
 /* rng.hpp:33-35 + :38 -- n uniform01 draws of stream `stream_id` of `seed` */
 void bbo_stream_uniform01(uint64_t seed, uint64_t stream_id, uint64_t n, double* out);
+/* RandomStream(seed).uniform01() x n, rng.hpp:30,38 */
+void bbo_plain_uniform01(uint64_t seed, uint64_t n, double* out);
 /* schedule_arrivals, simulator.hpp:174-185 */
 void bbo_generate_arrivals(uint64_t seed, double rate, uint64_t n, double* out);
 

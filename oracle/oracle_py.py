@@ -233,6 +233,16 @@ def stream_uniform01(lib, seed, stream_id, n):
     return out
 
 
+def acceptance_trace(n=20000, seed=424242):
+    """The long-tailed trace of acceptance.cpp:366-375: RandomStream(424242),
+    v = min((1-u)^(-1/1.2), 500)."""
+    lib = oracle()
+    u = np.empty(n)
+    lib.bbo_plain_uniform01.argtypes = [C.c_uint64, C.c_uint64, _dp]
+    lib.bbo_plain_uniform01(seed, n, u.ctypes.data_as(_dp))
+    return np.minimum(np.power(1.0 - u, -1.0 / 1.2), 500.0)
+
+
 def run_replicas(d: dict, master: int, rep0: int, nrep: int, threads: int):
     """Reference replications on `threads` host threads -> (per-rep metrics list, seconds)."""
     lib = reference()

@@ -53,6 +53,26 @@ __global__ void thresholds_kernel(GenPoint* pts, uint32_t n_points) {
     else s_above = lo;
   }
   __syncthreads();
+  // bucket lookup table over the top 8 key bits (53-bit keys only)
+  if (P.svc.key_domain == kKeyDomain53) {
+    __shared__ int s_multi;
+    if (threadIdx.x == 0) s_multi = 0;
+    __syncthreads();
+    for (uint32_t b = threadIdx.x; b < 256; b += blockDim.x) {
+      const uint64_t lo = (uint64_t)b << 45, hi = lo + (1ull << 45);
+      uint32_t c = 0, inside = 0;
+      for (uint32_t j = 1; j < k; ++j) {
+        c += P.thr[j] <= lo;
+        inside += P.thr[j] > lo && P.thr[j] < hi;
+      }
+      P.lut[b] = (uint8_t)c;
+      if (inside > 1) atomicOr(&s_multi, 1);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) P.lut_ok = !s_multi;
+  } else if (threadIdx.x == 0) {
+    P.lut_ok = 0;
+  }
   if (threadIdx.x == 0) {
     const uint64_t vlo = P.thr[0] > s_pos ? P.thr[0] : s_pos;
     if (s_above == 0) {  // every key is above the support
@@ -68,8 +88,12 @@ __global__ void thresholds_kernel(GenPoint* pts, uint32_t n_points) {
 }
 
 // 1 + #{j in 1..k-1 : thr[j] <= x}  (== assign_bin for monotone s(x))
-__device__ __forceinline__ uint32_t bin_of(const uint64_t* thr, uint32_t k, uint32_t top,
-                                           uint64_t x) {
+__device__ __forceinline__ uint32_t bin_of(const uint64_t* thr, const uint8_t* lut, bool lut_ok,
+                                           uint32_t k, uint32_t top, uint64_t x) {
+  if (lut_ok) {  // one table read + at most one threshold compare
+    const uint32_t c = lut[x >> 45];
+    return c + 1 + (c + 1 < k && thr[c + 1] <= x);
+  }
   uint32_t pos = 0;
   for (uint32_t step = top; step; step >>= 1)
     if (pos + step < k && thr[pos + step] <= x) pos += step;
@@ -125,6 +149,7 @@ template <int ERR, bool CYC, bool OVL>
 __global__ void __launch_bounds__(kGenThreads) gen_kernel(GenLaunch L) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ uint64_t s_thr[kGenWarps][BB_MAX_BINS + 1];
+  __shared__ __align__(16) uint8_t s_lut[kGenWarps][256];
   const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5, tid = threadIdx.x;
   const uint32_t kmax = L.k_max;
   uint64_t* st = reinterpret_cast<uint64_t*>(smem_raw);  // [kmax][T] packed (key<<11 | cnt)
@@ -146,6 +171,7 @@ __global__ void __launch_bounds__(kGenThreads) gen_kernel(GenLaunch L) {
     const GenPoint& P = L.pts_dev[p];
     const uint32_t k = P.k, B = P.B, n = P.n;
     for (uint32_t j = lane; j <= k; j += 32) s_thr[wib][j] = P.thr[j];
+    reinterpret_cast<uint2*>(s_lut[wib])[lane] = reinterpret_cast<const uint2*>(P.lut)[lane];
     __syncwarp();
     const uint32_t r = L.rep_begin + c * 32 + lane;
     if (r < L.rep_end) {
@@ -153,6 +179,8 @@ __global__ void __launch_bounds__(kGenThreads) gen_kernel(GenLaunch L) {
       const uint64_t sw = splitmix64(seed);  // RandomStream(seed) whitening, rng.hpp:30
       const uint32_t c2 = (uint32_t)sw, c3 = (uint32_t)(sw >> 32);
       const uint64_t* thr = s_thr[wib];
+      const uint8_t* lut = s_lut[wib];
+      const bool lut_ok = P.lut_ok != 0;
       const uint32_t top = k > 1 ? (1u << (31 - __clz(k - 1))) : 0u;
       const bool check = P.check_domain != 0;
       const uint64_t vlo = P.vlo, vhi = P.vhi;
@@ -174,7 +202,7 @@ __global__ void __launch_bounds__(kGenThreads) gen_kernel(GenLaunch L) {
         for (uint32_t i = 0; i < n; ++i) {
           const Draw d = draw<ERR, CYC>(P, i, c2, c3, ecache, cyc);
           // exponential inter-arrival, rng.hpp:43 / simulator.hpp:181
-          t += -log1p(-(double)d.xg * 0x1.0p-53) * inv_lambda;
+          t += exp1_from_bits53(d.xg) * inv_lambda;
           asum += t;
           if (i == 0) a0 = t;
           if (check && (d.xs < vlo || d.xs > vhi)) {
@@ -182,7 +210,7 @@ __global__ void __launch_bounds__(kGenThreads) gen_kernel(GenLaunch L) {
             failed = true;
             break;
           }
-          const uint32_t tb = k > 1 ? bin_of(thr, k, top, d.xs) : 1u;
+          const uint32_t tb = k > 1 ? bin_of(thr, lut, lut_ok, k, top, d.xs) : 1u;
           const uint32_t pb = ERR ? predict<ERR>(P, tb, k, d.xe) : tb;
           uint64_t* slot = st + (pb - 1) * kGenThreads + tid;
           const uint64_t s0 = *slot;
@@ -224,7 +252,7 @@ __global__ void __launch_bounds__(kGenThreads) gen_kernel(GenLaunch L) {
           busy_out = busy / mk_out;
           lat_out = (latw - (asum - leftover)) / (double)ncomp;
         } else {
-          mk_out = thr_out = busy_out = lat_out = failed ? CUDART_NAN : 0.0;
+          mk_out = thr_out = busy_out = lat_out = failed ? BB_QNAN : 0.0;
         }
       } else {
         // ------------------------------------------------------- overload
@@ -239,7 +267,7 @@ __global__ void __launch_bounds__(kGenThreads) gen_kernel(GenLaunch L) {
             failed = true;
             break;
           }
-          const uint32_t tb = k > 1 ? bin_of(thr, k, top, d.xs) : 1u;
+          const uint32_t tb = k > 1 ? bin_of(thr, lut, lut_ok, k, top, d.xs) : 1u;
           const uint32_t pb = ERR ? predict<ERR>(P, tb, k, d.xe) : tb;
           const uint32_t cnt = ++s_F[(pb - 1) * kGenThreads + tid];
           if (cnt == B) s_cf[(pb - 1) * kGenThreads + tid] = i;
@@ -260,7 +288,7 @@ __global__ void __launch_bounds__(kGenThreads) gen_kernel(GenLaunch L) {
           double busy = 0.0, latw = 0.0;
           for (uint32_t i = 0; i < n; ++i) {  // pass 2: same draws, batch positions
             const Draw d = draw<ERR, CYC>(P, i, c2, c3, ecache, cyc);
-            const uint32_t tb = k > 1 ? bin_of(thr, k, top, d.xs) : 1u;
+            const uint32_t tb = k > 1 ? bin_of(thr, lut, lut_ok, k, top, d.xs) : 1u;
             const uint32_t pb = ERR ? predict<ERR>(P, tb, k, d.xe) : tb;
             uint64_t* slot = st + (pb - 1) * kGenThreads + tid;
             const uint64_t s0 = *slot;
@@ -318,14 +346,14 @@ __global__ void __launch_bounds__(kGenThreads) gen_kernel(GenLaunch L) {
             mk_out = thr_out = busy_out = lat_out = 0.0;
           }
         } else {
-          mk_out = thr_out = busy_out = lat_out = CUDART_NAN;
+          mk_out = thr_out = busy_out = lat_out = BB_QNAN;
         }
       }
       const uint64_t o = (uint64_t)P.gidx * L.reps_total + r;
       L.out[BB_REP_THROUGHPUT * stride + o] = thr_out;
       L.out[BB_REP_LATENCY * stride + o] = lat_out;
-      L.out[BB_REP_P50 * stride + o] = CUDART_NAN;  // generated mode: not tracked (SURVEY §7 hard part 4)
-      L.out[BB_REP_P99 * stride + o] = CUDART_NAN;
+      L.out[BB_REP_P50 * stride + o] = BB_QNAN;  // generated mode: not tracked (SURVEY §7 hard part 4)
+      L.out[BB_REP_P99 * stride + o] = BB_QNAN;
       L.out[BB_REP_MAKESPAN * stride + o] = mk_out;
       L.out[BB_REP_BUSY * stride + o] = busy_out;
     }

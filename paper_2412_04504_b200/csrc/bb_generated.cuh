@@ -20,6 +20,10 @@ struct GenPoint {
   const uint64_t* conf_thr; // confusion: k*k cumulative thresholds (device)
   const uint32_t* cyc_rank; // cyclic: sorted rank of lengths[j] (device)
   uint64_t thr[BB_MAX_BINS + 1];  // thr[j], j=1..k-1: bin > j <=> x >= thr[j]
+  // bin lookup: lut[x >> 45] = #{j : thr[j] <= bucket start}; valid when no
+  // 2^45-wide key bucket holds two thresholds (then one compare finishes)
+  uint8_t lut[256];
+  uint32_t lut_ok;
 };
 
 struct GenLaunch {

@@ -20,7 +20,7 @@ __global__ void draw_kernel(MatArgs M) {
   if (i >= M.n) return;
   const uint4 r = philox(i, kStreamArrivalService, M.c2, M.c3);
   const uint64_t xg = bits53(r.x, r.y);
-  M.gap[i] = M.overload ? 0.0 : -log1p(-(double)xg * 0x1.0p-53) * M.inv_lambda;
+  M.gap[i] = M.overload ? 0.0 : exp1_from_bits53(xg) * M.inv_lambda;
   uint64_t xs;
   if (M.svc.kind == kSvcCyclic) xs = M.cyc_rank[i % M.svc.n_table];
   else xs = bits53(r.z, r.w);

@@ -695,7 +695,7 @@ __global__ void __launch_bounds__(256) request_kernel(QArgs Q) {
   if (i < Q.n) {
     const uint32_t b = Q.pb8[i];
     unsigned long long key = KEY_UNSERVED;
-    double comp = CUDART_NAN;
+    double comp = BB_QNAN;
     uint32_t bid = BB_NO_BATCH;
     if (b) {
       const uint32_t r = Q.rank[i];
@@ -983,32 +983,33 @@ void trace_run(const TraceArgs& A, TraceResult* R, cudaStream_t s) {
     R->n_batches = nb;
     R->n_completed = info.nc;
     for (uint32_t b = 0; b < k; ++b) R->per_bin[b] = info.nbat[b];
-    if (nb == 0) goto cleanup;  // nothing served: metrics stay zero (finish(), :283)
-    BB_CK(pool.alloc((void**)&map, (size_t)nb * 4));
-    BB_CK(pool.alloc((void**)&order, (size_t)nb * 4));
-    BB_CK(pool.alloc((void**)&dfirst, (size_t)nb * 4));
-    BB_CK(pool.alloc((void**)&dR, (size_t)nb * 8));
-    BB_CK(pool.alloc((void**)&dS, (size_t)nb * 8));
-    BB_CK(pool.alloc((void**)&split, nb));
+    // nb == 0 (nothing served, finish() :283) still runs the request pass so
+    // every request reports kNoBatch / NaN completion
+    BB_CK(pool.alloc((void**)&map, (size_t)nb * 4 + 4));
+    BB_CK(pool.alloc((void**)&order, (size_t)nb * 4 + 4));
+    BB_CK(pool.alloc((void**)&dfirst, (size_t)nb * 4 + 4));
+    BB_CK(pool.alloc((void**)&dR, (size_t)nb * 8 + 8));
+    BB_CK(pool.alloc((void**)&dS, (size_t)nb * 8 + 8));
+    BB_CK(pool.alloc((void**)&split, nb + 1));
     start = A.bat_start;
     finish = A.bat_finish;
-    if (!start) BB_CK(pool.alloc((void**)&start, (size_t)nb * 8));
-    if (!finish) BB_CK(pool.alloc((void**)&finish, (size_t)nb * 8));
-    if (info.path == 1) {
+    if (!start) BB_CK(pool.alloc((void**)&start, (size_t)nb * 8 + 8));
+    if (!finish) BB_CK(pool.alloc((void**)&finish, (size_t)nb * 8 + 8));
+    if (info.path == 1 && info.nclose) {
       ovl_first_kernel<<<grid_for(info.nclose, 256), 256, 0, s>>>(ws, info.nclose);
       note_launch();
       BB_CK(cudaGetLastError());
     }
-    order_kernel<<<grid_for(nb, 256), 256, 0, s>>>(ws, map, order, dfirst, k, B, A.flush,
+    if (nb) order_kernel<<<grid_for(nb, 256), 256, 0, s>>>(ws, map, order, dfirst, k, B, A.flush,
                                                    (int32_t)info.path);
     note_launch();
     BB_CK(cudaGetLastError());
-    gather_kernel<<<grid_for(nb, 256), 256, 0, s>>>(ws, order, (int32_t)info.path, B, dR, dS,
+    if (nb) gather_kernel<<<grid_for(nb, 256), 256, 0, s>>>(ws, order, (int32_t)info.path, B, dR, dS,
                                                     A.bat_bin, A.bat_size);
     note_launch();
     BB_CK(cudaGetLastError());
     // Lindley: certified busy-period splits, then exact serial segments
-    const uint32_t lt = (nb + LTILE - 1) / LTILE;
+    const uint32_t lt = nb ? (nb + LTILE - 1) / LTILE : 1;
     double *aggA, *aggC, *incA, *incC, *busy_part, *busy_sum;
     uint32_t* lflag;
     BB_CK(pool.alloc((void**)&aggA, (size_t)lt * 8));
@@ -1022,14 +1023,14 @@ void trace_run(const TraceArgs& A, TraceResult* R, cudaStream_t s) {
     {
       LArgs L{dR, dS, nb, split, busy_part, aggA, aggC, incA, incC, lflag, ws.counters + 1,
               (double)(nb + 4096) * 0x1.0p-50};
-      lindley_scan_kernel<<<lt, LB, 0, s>>>(L);
+      if (nb) lindley_scan_kernel<<<lt, LB, 0, s>>>(L);
       note_launch();
       BB_CK(cudaGetLastError());
     }
-    lindley_segments_kernel<<<grid_for(nb, 128), 128, 0, s>>>(dR, dS, split, nb, start, finish);
+    if (nb) lindley_segments_kernel<<<grid_for(nb, 128), 128, 0, s>>>(dR, dS, split, nb, start, finish);
     note_launch();
     BB_CK(cudaGetLastError());
-    sum_kernel<<<1, 256, 0, s>>>(busy_part, lt, busy_sum);
+    sum_kernel<<<1, 256, 0, s>>>(busy_part, nb ? lt : 0, busy_sum);
     note_launch();
     BB_CK(cudaGetLastError());
     // per-request pass
@@ -1074,7 +1075,7 @@ void trace_run(const TraceArgs& A, TraceResult* R, cudaStream_t s) {
     if (A.bat_first) BB_CK(cudaMemcpyAsync(A.bat_first, dfirst, (size_t)nb * 4, cudaMemcpyDeviceToDevice, s));
     double last = 0, a0 = 0, busy = 0, lsum = 0;
     unsigned long long mm[2];
-    BB_CK(cudaMemcpyAsync(&last, finish + nb - 1, 8, cudaMemcpyDeviceToHost, s));
+    if (nb) BB_CK(cudaMemcpyAsync(&last, finish + nb - 1, 8, cudaMemcpyDeviceToHost, s));
     BB_CK(cudaMemcpyAsync(&a0, A.a, 8, cudaMemcpyDeviceToHost, s));
     BB_CK(cudaMemcpyAsync(&busy, busy_sum, 8, cudaMemcpyDeviceToHost, s));
     BB_CK(cudaMemcpyAsync(&lsum, lat_sum, 8, cudaMemcpyDeviceToHost, s));

@@ -146,8 +146,7 @@ def test_confusion_and_exponential_vs_reference():
 
 def test_trace_replay_generated_monotone_in_k():
     # acceptance criterion 10: Pareto-like trace, B=32, overload, resample
-    rs = np.random.default_rng(424242)
-    trace = np.minimum((1.0 - rs.random(20000)) ** (-1.0 / 1.2), 500.0).tolist()
+    trace = O.acceptance_trace().tolist()  # acceptance.cpp:366-375, the reference's own trace
     base = bb.RunTemplate(n_requests=12800, batch_size=32, flush_partial=False,
                           service=bb.ServiceSpec("trace", trace_times=trace, trace_mode="resample"))
     spec = bb.ExperimentSpec(base=base, axes=[bb.SweepAxis("k", [1, 2, 4, 8, 16, 32])],
@@ -155,9 +154,18 @@ def test_trace_replay_generated_monotone_in_k():
     pts = bb.run_experiment(spec)
     thr = [p.throughput_mean for p in pts]
     assert all(b >= a * (1 - 1e-9) for a, b in zip(thr, thr[1:]))
-    # reference curve (proj/test_output.txt:26) within a few percent at 20x the replications
-    for p, want in zip(pts, [0.6538, 0.807, 1.009, 1.338, 1.751, 2.355]):
-        assert abs(p.throughput_mean - want) / want < 0.03
+    # 3 standard errors against the reference's own replications (the
+    # published 10-replication curve, proj/test_output.txt:26, is itself
+    # noisy for this heavy-tailed trace; its exact reproduction is checked
+    # bit-for-bit in test_gpu_reference_rng.py)
+    for p in pts:
+        if p.k not in (1, 8, 32):
+            continue
+        edges = bb.empirical_boundaries(p.k, trace).edges
+        ref, _ = ref_stats(dict(arrival_rate=math.inf, n_requests=12800, batch_size=32,
+                                edges=edges, flush_partial=False, service="trace_resample",
+                                table=trace), 400)
+        assert within_3se(p.throughput_mean, p.throughput_std, 200, ref)
 
 
 def test_fused_replica_equals_single_run_on_same_streams():

@@ -74,8 +74,7 @@ def test_run_simulation_detailed_matches_reference_binary(i):
 
 def test_replay_trace_resample_matches_reference():
     # acceptance.cpp criterion 10 setting (Pareto-like trace, B=32, overload, resample)
-    rs = np.random.default_rng(424242)
-    trace = np.minimum((1.0 - rs.random(20000)) ** (-1.0 / 1.2), 500.0)
+    trace = O.acceptance_trace()  # acceptance.cpp:366-375
     for k in (1, 4, 16, 32):
         edges = bb.empirical_boundaries(k, trace).edges
         seed = bb.replication_seed(1001, 3)
@@ -113,3 +112,15 @@ def test_run_experiment_reference_streams_bit_exact_throughput():
             mean += x
         mean /= 10
         assert same_bits(p.throughput_mean, mean)
+
+
+def test_acceptance_criterion10_curve_exact():
+    # acceptance.cpp:366-395 with the reference's streams: the published
+    # curve 0.6538 0.807 1.009 1.338 1.751 2.355 (proj/test_output.txt:26)
+    trace = O.acceptance_trace().tolist()
+    base = bb.RunTemplate(n_requests=12800, batch_size=32, flush_partial=False,
+                          service=bb.ServiceSpec("trace", trace_times=trace, trace_mode="resample"))
+    spec = bb.ExperimentSpec(base=base, axes=[bb.SweepAxis("k", [1, 2, 4, 8, 16, 32])],
+                             replications=10, seed=1001, rng="reference")
+    got = [f"{p.throughput_mean:.4g}" for p in bb.run_experiment(spec)]
+    assert got == ["0.6538", "0.807", "1.009", "1.338", "1.751", "2.355"]
