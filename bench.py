@@ -215,7 +215,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--reps", type=int, default=10_000, help="replications per point per GPU")
     ap.add_argument("--requests", type=int, default=100_000)
-    ap.add_argument("--ref-reps", type=int, default=2)
+    ap.add_argument("--ref-reps", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-trace", action="store_true")
     args = ap.parse_args()

@@ -72,6 +72,9 @@ BB_HD uint64_t replication_seed(uint64_t master, uint64_t rep) {
 enum : uint32_t { kStreamArrivalService = 0, kStreamError = 1 };
 
 // ------------------------------------------------------ exponential variate
+__constant__ const double kAtanhC[10] = {1.0 / 21, 1.0 / 19, 1.0 / 17, 1.0 / 15, 1.0 / 13,
+                                         1.0 / 11, 1.0 / 9,  1.0 / 7,  1.0 / 5,  1.0 / 3};
+
 // E = -log1p(-u) with u = x * 2^-53 (the reference's draw, rng.hpp:43).
 // 1 - u = (2^53 - x) * 2^-53 is exact, so E = -log(y) + 53 ln2 with the
 // integer y = 2^53 - x in [1, 2^53].  Branch-free: exponent split, reduction
@@ -98,16 +101,11 @@ __device__ __forceinline__ double exp1_from_bits53(uint64_t x) {
   double s = num * r;
   s = fma(fma(-den, s, num), r, s);
   const double s2 = s * s;
-  double p = 1.0 / 21;
-  p = fma(p, s2, 1.0 / 19);
-  p = fma(p, s2, 1.0 / 17);
-  p = fma(p, s2, 1.0 / 15);
-  p = fma(p, s2, 1.0 / 13);
-  p = fma(p, s2, 1.0 / 11);
-  p = fma(p, s2, 1.0 / 9);
-  p = fma(p, s2, 1.0 / 7);
-  p = fma(p, s2, 1.0 / 5);
-  p = fma(p, s2, 1.0 / 3);
+  // atanh series coefficients 1/(2j+1), j = 10..1, from the constant bank
+  // (DFMA takes a c[] operand: no per-coefficient register moves)
+  double p = kAtanhC[0];
+#pragma unroll
+  for (int j = 1; j < 10; ++j) p = fma(p, s2, kAtanhC[j]);
   const double logm = fma(2.0 * s * s2, p, 2.0 * s);
   constexpr double kLn2Hi = 6.93147180369123816490e-01, kLn2Lo = 1.90821492927058770002e-10;
   const double k = (double)(53 - e);  // E = (53 - e) ln2 - log(m)
@@ -159,6 +157,28 @@ __device__ __forceinline__ double svc_of_key(const SvcParams& p, uint64_t x) {
     }
     default:  // kSvcCyclic
       return p.table[x];
+  }
+}
+
+// Same, with the kind fixed at compile time (the fused kernel's closures).
+template <int KIND>
+__device__ __forceinline__ double svc_of_key_t(const SvcParams& p, uint64_t x) {
+  if (KIND == kSvcUniform) {
+    const double u = (double)x * 0x1.0p-53;
+    return __dadd_rn(p.lo, __dmul_rn(__dsub_rn(p.hi, p.lo), u));
+  } else if (KIND == kSvcLinear) {
+    const double u = (double)x * 0x1.0p-53;
+    const double len = __dadd_rn(p.lo, __dmul_rn(__dsub_rn(p.hi, p.lo), u));
+    return __dadd_rn(__dmul_rn(p.lin_b, len), p.lin_a);
+  } else if (KIND == kSvcExponential) {
+    return exp1_from_bits53(x) / p.rate;
+  } else if (KIND == kSvcLogNormal) {
+    const double u = ((double)x + 0.5) * 0x1.0p-53;
+    return exp(p.mu + p.sigma * normcdfinv(u));
+  } else if (KIND == kSvcTable) {
+    return p.table[__umul64hi(x << 11, (uint64_t)p.n_table)];
+  } else {
+    return p.table[x];
   }
 }
 

@@ -122,30 +122,52 @@ __device__ __forceinline__ uint32_t predict(const GenPoint& P, uint32_t tb, uint
 struct Draw {
   uint64_t xg;  // inter-arrival uniform (53-bit)
   uint64_t xs;  // service key
-  uint64_t xe;  // error uniform (53-bit)
 };
 
-template <int ERR, bool CYC>
-__device__ __forceinline__ Draw draw(const GenPoint& P, uint32_t i, uint32_t c2, uint32_t c3,
-                                     uint4& ecache, uint32_t& cyc) {
+template <int SVC>
+__device__ __forceinline__ Draw draw(const uint32_t* __restrict__ cyc_rank, uint32_t n_table,
+                                     uint32_t i, uint32_t c2, uint32_t c3, uint32_t& cyc) {
   Draw d;
   const uint4 r = philox(i, kStreamArrivalService, c2, c3);
   d.xg = bits53(r.x, r.y);
-  if (CYC) {
-    d.xs = P.cyc_rank[cyc];
-    if (++cyc == P.svc.n_table) cyc = 0;
+  if (SVC == kSvcCyclic) {
+    d.xs = cyc_rank[cyc];
+    if (++cyc == n_table) cyc = 0;
   } else {
     d.xs = bits53(r.z, r.w);
-  }
-  d.xe = 0;
-  if (ERR != 0) {
-    if ((i & 1u) == 0) ecache = philox(i >> 1, kStreamError, c2, c3);
-    d.xe = (i & 1u) ? bits53(ecache.z, ecache.w) : bits53(ecache.x, ecache.y);
   }
   return d;
 }
 
-template <int ERR, bool CYC, bool OVL>
+// Per-replication state of the finite-rate simulation (registers).
+struct Rep {
+  double t, D, busy, latw, asum;
+  uint64_t ncomp;
+};
+
+// One request folded into its bin; closes the batch at B members
+// (on_arrival + form_batch + dispatch, simulator.hpp:187-267, one server).
+template <int SVC>
+__device__ __forceinline__ void fold(Rep& R, uint64_t* __restrict__ slot, double* __restrict__ osum,
+                                     bool track, uint64_t xs, uint32_t B, const SvcParams& svc) {
+  const uint64_t s0 = *slot;
+  const uint64_t km = max(s0 & ~kCntMask, xs << kCntBits);
+  const uint32_t cnt = (uint32_t)(s0 & kCntMask) + 1;
+  if (cnt == B) {
+    *slot = 0;
+    const double S = svc_of_key_t<SVC>(svc, km >> kCntBits);
+    R.D = __dadd_rn(fmax(R.D, R.t), S);
+    R.busy += S;
+    R.latw += (double)B * R.D;
+    R.ncomp += B;
+    if (track) *osum = 0.0;
+  } else {
+    *slot = km | cnt;
+    if (track) *osum += R.t;
+  }
+}
+
+template <int SVC, int ERR, bool OVL>
 __global__ void __launch_bounds__(kGenThreads) gen_kernel(GenLaunch L) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ uint64_t s_thr[kGenWarps][BB_MAX_BINS + 1];
@@ -178,18 +200,49 @@ __global__ void __launch_bounds__(kGenThreads) gen_kernel(GenLaunch L) {
       const uint64_t seed = L.single_seed ? L.master : replication_seed(L.master, r);
       const uint64_t sw = splitmix64(seed);  // RandomStream(seed) whitening, rng.hpp:30
       const uint32_t c2 = (uint32_t)sw, c3 = (uint32_t)(sw >> 32);
+      // point parameters in registers (the closures read them, not global memory)
+      const SvcParams svc = P.svc;
+      const uint32_t* __restrict__ cyc_rank = P.cyc_rank;
+      const uint64_t* __restrict__ conf_thr = P.conf_thr;
       const uint64_t* thr = s_thr[wib];
       const uint8_t* lut = s_lut[wib];
       const bool lut_ok = P.lut_ok != 0;
       const uint32_t top = k > 1 ? (1u << (31 - __clz(k - 1))) : 0u;
       const bool check = P.check_domain != 0;
-      const uint64_t vlo = P.vlo, vhi = P.vhi;
+      const uint64_t vlo = P.vlo, vhi = P.vhi, et1 = P.e_t1, et2 = P.e_t2;
       const bool flush = P.flush != 0;
+      const uint32_t nt = svc.n_table;
       for (uint32_t b = 0; b < k; ++b) st[b * kGenThreads + tid] = 0;
-      uint4 ecache = make_uint4(0, 0, 0, 0);
       uint32_t cyc = 0;
       bool failed = false;
       double thr_out, lat_out, mk_out, busy_out;
+
+      // bin of a key, then the error model (predict_bin, binning.hpp:231-261)
+      auto bin_pred = [&](uint64_t xs, uint64_t xe) -> uint32_t {
+        const uint32_t tb = k > 1 ? bin_of(thr, lut, lut_ok, k, top, xs) : 1u;
+        if (ERR == 1) {
+          if (tb == 1) return xe < et1 ? 2u : 1u;
+          if (tb == k) return xe < et1 ? k - 1 : k;
+          if (xe < et1) return tb - 1;
+          if (xe >= et2) return tb + 1;
+          return tb;
+        } else if (ERR == 2) {
+          const uint64_t* row = conf_thr + (uint64_t)(tb - 1) * k;
+          uint32_t pb = 1;
+          for (uint32_t j = 0; j + 1 < k; ++j) pb += xe >= row[j];
+          return pb;
+        }
+        return tb;
+      };
+      // the error stream's two uniforms for requests (2m, 2m+1)
+      auto err_pair = [&](uint32_t i, uint64_t& e0, uint64_t& e1) {
+        if (ERR != 0) {
+          const uint4 e = philox(i >> 1, kStreamError, c2, c3);
+          e0 = bits53(e.x, e.y);
+          e1 = bits53(e.z, e.w);
+        }
+      };
+      auto out_of_support = [&](uint64_t xs) { return check && (xs < vlo || xs > vhi); };
 
       if (!OVL) {
         // ------------------------------------------------ finite arrival rate
@@ -197,36 +250,49 @@ __global__ void __launch_bounds__(kGenThreads) gen_kernel(GenLaunch L) {
         const bool track = !flush;
         if (track)
           for (uint32_t b = 0; b < k; ++b) s_osum[b * kGenThreads + tid] = 0.0;
-        double t = 0.0, D = 0.0, busy = 0.0, latw = 0.0, asum = 0.0, a0 = 0.0;
-        uint64_t ncomp = 0;
-        for (uint32_t i = 0; i < n; ++i) {
-          const Draw d = draw<ERR, CYC>(P, i, c2, c3, ecache, cyc);
-          // exponential inter-arrival, rng.hpp:43 / simulator.hpp:181
-          t += exp1_from_bits53(d.xg) * inv_lambda;
-          asum += t;
-          if (i == 0) a0 = t;
-          if (check && (d.xs < vlo || d.xs > vhi)) {
-            raise_error(L.err, i, BB_EDOMAIN, svc_of_key(P.svc, d.xs), r);
+        Rep R{0.0, 0.0, 0.0, 0.0, 0.0, 0};
+        uint32_t cyc0 = 0;
+        const double a0 = exp1_from_bits53(draw<SVC>(cyc_rank, nt, 0, c2, c3, cyc0).xg) * inv_lambda;
+        // two requests per iteration: both draws, exponentials and bins are
+        // independent, so their latencies overlap; the folds stay in order
+        uint32_t i = 0;
+        for (; i + 2 <= n; i += 2) {
+          const Draw d0 = draw<SVC>(cyc_rank, nt, i, c2, c3, cyc);
+          const Draw d1 = draw<SVC>(cyc_rank, nt, i + 1, c2, c3, cyc);
+          uint64_t e0 = 0, e1 = 0;
+          err_pair(i, e0, e1);
+          const double g0 = exp1_from_bits53(d0.xg) * inv_lambda;
+          const double g1 = exp1_from_bits53(d1.xg) * inv_lambda;
+          if (out_of_support(d0.xs) || out_of_support(d1.xs)) {
+            const uint32_t bad = out_of_support(d0.xs) ? i : i + 1;
+            raise_error(L.err, bad, BB_EDOMAIN,
+                        svc_of_key_t<SVC>(svc, bad == i ? d0.xs : d1.xs), r);
             failed = true;
             break;
           }
-          const uint32_t tb = k > 1 ? bin_of(thr, lut, lut_ok, k, top, d.xs) : 1u;
-          const uint32_t pb = ERR ? predict<ERR>(P, tb, k, d.xe) : tb;
-          uint64_t* slot = st + (pb - 1) * kGenThreads + tid;
-          const uint64_t s0 = *slot;
-          const uint64_t km = max(s0 & ~kCntMask, d.xs << kCntBits);
-          const uint32_t cnt = (uint32_t)(s0 & kCntMask) + 1;
-          if (cnt == B) {  // form_batch + dispatch, simulator.hpp:237-267
-            *slot = 0;
-            const double S = svc_of_key(P.svc, km >> kCntBits);
-            D = __dadd_rn(fmax(D, t), S);
-            busy += S;
-            latw += (double)B * D;
-            ncomp += B;
-            if (track) s_osum[(pb - 1) * kGenThreads + tid] = 0.0;
+          const uint32_t p0 = bin_pred(d0.xs, e0), p1 = bin_pred(d1.xs, e1);
+          R.t += g0;  // exponential inter-arrival, simulator.hpp:181
+          R.asum += R.t;
+          fold<SVC>(R, st + (p0 - 1) * kGenThreads + tid, s_osum + (p0 - 1) * kGenThreads + tid,
+                    track, d0.xs, B, svc);
+          R.t += g1;
+          R.asum += R.t;
+          fold<SVC>(R, st + (p1 - 1) * kGenThreads + tid, s_osum + (p1 - 1) * kGenThreads + tid,
+                    track, d1.xs, B, svc);
+        }
+        if (!failed && i < n) {
+          const Draw d0 = draw<SVC>(cyc_rank, nt, i, c2, c3, cyc);
+          uint64_t e0 = 0, e1 = 0;
+          err_pair(i, e0, e1);
+          if (out_of_support(d0.xs)) {
+            raise_error(L.err, i, BB_EDOMAIN, svc_of_key_t<SVC>(svc, d0.xs), r);
+            failed = true;
           } else {
-            *slot = km | cnt;
-            if (track) s_osum[(pb - 1) * kGenThreads + tid] += t;
+            const uint32_t p0 = bin_pred(d0.xs, e0);
+            R.t += exp1_from_bits53(d0.xg) * inv_lambda;
+            R.asum += R.t;
+            fold<SVC>(R, st + (p0 - 1) * kGenThreads + tid, s_osum + (p0 - 1) * kGenThreads + tid,
+                      track, d0.xs, B, svc);
           }
         }
         double leftover = 0.0;
@@ -236,21 +302,21 @@ __global__ void __launch_bounds__(kGenThreads) gen_kernel(GenLaunch L) {
             const uint32_t cnt = (uint32_t)(s0 & kCntMask);
             if (!cnt) continue;
             if (flush) {  // on_drain partials at the last arrival, bin order
-              const double S = svc_of_key(P.svc, s0 >> kCntBits);
-              D = __dadd_rn(fmax(D, t), S);
-              busy += S;
-              latw += (double)cnt * D;
-              ncomp += cnt;
+              const double S = svc_of_key_t<SVC>(svc, s0 >> kCntBits);
+              R.D = __dadd_rn(fmax(R.D, R.t), S);
+              R.busy += S;
+              R.latw += (double)cnt * R.D;
+              R.ncomp += cnt;
             } else {
               leftover += s_osum[b * kGenThreads + tid];
             }
           }
         }
-        if (!failed && ncomp > 0) {  // finish(), simulator.hpp:279-301
-          mk_out = D - a0;
-          thr_out = (double)ncomp / mk_out;
-          busy_out = busy / mk_out;
-          lat_out = (latw - (asum - leftover)) / (double)ncomp;
+        if (!failed && R.ncomp > 0) {  // finish(), simulator.hpp:279-301
+          mk_out = R.D - a0;
+          thr_out = (double)R.ncomp / mk_out;
+          busy_out = R.busy / mk_out;
+          lat_out = (R.latw - (R.asum - leftover)) / (double)R.ncomp;
         } else {
           mk_out = thr_out = busy_out = lat_out = failed ? BB_QNAN : 0.0;
         }
@@ -260,15 +326,16 @@ __global__ void __launch_bounds__(kGenThreads) gen_kernel(GenLaunch L) {
           s_F[b * kGenThreads + tid] = 0;
           s_cf[b * kGenThreads + tid] = 0xFFFFFFFFu;
         }
+        uint64_t e0 = 0, e1 = 0;
         for (uint32_t i = 0; i < n; ++i) {  // pass 1: per-bin totals, first closings
-          const Draw d = draw<ERR, CYC>(P, i, c2, c3, ecache, cyc);
-          if (check && (d.xs < vlo || d.xs > vhi)) {
-            raise_error(L.err, i, BB_EDOMAIN, svc_of_key(P.svc, d.xs), r);
+          const Draw d = draw<SVC>(cyc_rank, nt, i, c2, c3, cyc);
+          if ((i & 1u) == 0) err_pair(i, e0, e1);
+          if (out_of_support(d.xs)) {
+            raise_error(L.err, i, BB_EDOMAIN, svc_of_key_t<SVC>(svc, d.xs), r);
             failed = true;
             break;
           }
-          const uint32_t tb = k > 1 ? bin_of(thr, lut, lut_ok, k, top, d.xs) : 1u;
-          const uint32_t pb = ERR ? predict<ERR>(P, tb, k, d.xe) : tb;
+          const uint32_t pb = bin_pred(d.xs, (i & 1u) ? e1 : e0);
           const uint32_t cnt = ++s_F[(pb - 1) * kGenThreads + tid];
           if (cnt == B) s_cf[(pb - 1) * kGenThreads + tid] = i;
         }
@@ -287,9 +354,9 @@ __global__ void __launch_bounds__(kGenThreads) gen_kernel(GenLaunch L) {
           cyc = 0;
           double busy = 0.0, latw = 0.0;
           for (uint32_t i = 0; i < n; ++i) {  // pass 2: same draws, batch positions
-            const Draw d = draw<ERR, CYC>(P, i, c2, c3, ecache, cyc);
-            const uint32_t tb = k > 1 ? bin_of(thr, lut, lut_ok, k, top, d.xs) : 1u;
-            const uint32_t pb = ERR ? predict<ERR>(P, tb, k, d.xe) : tb;
+            const Draw d = draw<SVC>(cyc_rank, nt, i, c2, c3, cyc);
+            if ((i & 1u) == 0) err_pair(i, e0, e1);
+            const uint32_t pb = bin_pred(d.xs, (i & 1u) ? e1 : e0);
             uint64_t* slot = st + (pb - 1) * kGenThreads + tid;
             const uint64_t s0 = *slot;
             const uint64_t km = max(s0 & ~kCntMask, d.xs << kCntBits);
@@ -300,13 +367,13 @@ __global__ void __launch_bounds__(kGenThreads) gen_kernel(GenLaunch L) {
               const uint32_t j = s_jd[b * kGenThreads + tid]++;
               const uint32_t cfb = s_cf[b * kGenThreads + tid];
               uint64_t before;
-              if (flush && j > 0) {  // drain phase, bins in order
+              if (flush && j > 0) {  // drain phase, bins in order (on_drain, :218-221)
                 before = (uint64_t)B * Z + (uint64_t)B * (j - 1);
                 for (uint32_t q = 0; q < b; ++q) {
                   const uint32_t F = s_F[q * kGenThreads + tid];
                   before += (uint64_t)B * (F ? F - 1 : 0) + s_rem[q * kGenThreads + tid];
                 }
-              } else {  // round j, first-closing order
+              } else {  // round j, first-closing order (on_formation, :208-216)
                 uint64_t pos = 0;
                 for (uint32_t q = 0; q < k; ++q) {
                   const uint32_t F = s_F[q * kGenThreads + tid];
@@ -316,7 +383,7 @@ __global__ void __launch_bounds__(kGenThreads) gen_kernel(GenLaunch L) {
                 }
                 before = (uint64_t)B * pos;
               }
-              const double S = svc_of_key(P.svc, km >> kCntBits);
+              const double S = svc_of_key_t<SVC>(svc, km >> kCntBits);
               busy += S;
               latw += S * (double)(nc - before);
             } else {
@@ -330,7 +397,7 @@ __global__ void __launch_bounds__(kGenThreads) gen_kernel(GenLaunch L) {
               const uint32_t rem = s_rem[b * kGenThreads + tid];
               base += (uint64_t)B * (F ? F - 1 : 0);
               if (rem) {
-                const double S = svc_of_key(P.svc, st[b * kGenThreads + tid] >> kCntBits);
+                const double S = svc_of_key_t<SVC>(svc, st[b * kGenThreads + tid] >> kCntBits);
                 busy += S;
                 latw += S * (double)(nc - base);
               }
@@ -390,11 +457,12 @@ __global__ void point_reduce_kernel(const double* __restrict__ rep, uint32_t n_p
   }
 }
 
-template <int ERR, bool CYC, bool OVL>
+
+template <int SVC, int ERR, bool OVL>
 cudaError_t launch_gen(const GenLaunch& L, cudaStream_t s) {
   const size_t per = OVL ? (8 + 16) : 16;  // packed state + open sums | overload tables
   const size_t smem = (size_t)L.k_max * kGenThreads * per;
-  auto kern = gen_kernel<ERR, CYC, OVL>;
+  auto kern = gen_kernel<SVC, ERR, OVL>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 0, occ = 0;
@@ -414,6 +482,17 @@ cudaError_t launch_gen(const GenLaunch& L, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+template <int SVC>
+cudaError_t launch_svc(const GenLaunch& L, cudaStream_t s) {
+  const bool o = L.overload != 0;
+  switch (L.err_kind) {
+    case 0: return o ? launch_gen<SVC, 0, true>(L, s) : launch_gen<SVC, 0, false>(L, s);
+    case 1: return o ? launch_gen<SVC, 1, true>(L, s) : launch_gen<SVC, 1, false>(L, s);
+    case 2: return o ? launch_gen<SVC, 2, true>(L, s) : launch_gen<SVC, 2, false>(L, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
 }  // namespace
 
 cudaError_t gen_setup_thresholds(GenPoint* pts_dev, uint32_t n_points, cudaStream_t s) {
@@ -424,13 +503,14 @@ cudaError_t gen_setup_thresholds(GenPoint* pts_dev, uint32_t n_points, cudaStrea
 }
 
 cudaError_t gen_run(const GenLaunch& L, cudaStream_t s) {
-#define BB_GEN_CASE(E, C, O) \
-  if (L.err_kind == E && (L.cyclic != 0) == C && (L.overload != 0) == O) return launch_gen<E, C, O>(L, s);
-  BB_GEN_CASE(0, false, false) BB_GEN_CASE(1, false, false) BB_GEN_CASE(2, false, false)
-  BB_GEN_CASE(0, true, false) BB_GEN_CASE(1, true, false) BB_GEN_CASE(2, true, false)
-  BB_GEN_CASE(0, false, true) BB_GEN_CASE(1, false, true) BB_GEN_CASE(2, false, true)
-  BB_GEN_CASE(0, true, true) BB_GEN_CASE(1, true, true) BB_GEN_CASE(2, true, true)
-#undef BB_GEN_CASE
+  switch (L.svc_kind) {
+    case kSvcUniform: return launch_svc<kSvcUniform>(L, s);
+    case kSvcLinear: return launch_svc<kSvcLinear>(L, s);
+    case kSvcExponential: return launch_svc<kSvcExponential>(L, s);
+    case kSvcLogNormal: return launch_svc<kSvcLogNormal>(L, s);
+    case kSvcTable: return launch_svc<kSvcTable>(L, s);
+    case kSvcCyclic: return launch_svc<kSvcCyclic>(L, s);
+  }
   return cudaErrorInvalidValue;
 }
 

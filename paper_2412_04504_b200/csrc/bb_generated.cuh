@@ -37,6 +37,7 @@ struct GenLaunch {
   uint32_t rep_begin, rep_end;
   int32_t err_kind;
   int32_t cyclic;
+  int32_t svc_kind;          // SvcKind of every point in this launch
   int32_t overload;
   double* out;              // [BB_REP_FIELDS][n_points*reps_total]
   DevError* err;

@@ -940,8 +940,7 @@ void launch_sweep(const SweepParams* E, Sweep& W, uint64_t rep_begin, uint64_t r
   };
   std::vector<Key> keys(P);
   for (size_t i = 0; i < P; ++i)
-    keys[i] = Key{(int)W.gp[i].err_kind, W.gp[i].svc.kind == bb::kSvcCyclic,
-                  W.gp[i].inv_lambda == 0.0};
+    keys[i] = Key{(int)W.gp[i].err_kind, (int)W.gp[i].svc.kind, W.gp[i].inv_lambda == 0.0};
   std::vector<bool> done(P, false);
   bool first = true;
   for (size_t i = 0; i < P; ++i) {
@@ -978,7 +977,8 @@ void launch_sweep(const SweepParams* E, Sweep& W, uint64_t rep_begin, uint64_t r
     L.rep_begin = (uint32_t)rep_begin;
     L.rep_end = (uint32_t)rep_end;
     L.err_kind = keys[i].err;
-    L.cyclic = keys[i].cyc;
+    L.cyclic = keys[i].cyc == bb::kSvcCyclic;
+    L.svc_kind = keys[i].cyc;
     L.overload = keys[i].ovl;
     L.out = rep_dev;
     DBuf err(sizeof(bb::DevError), st);
