@@ -84,7 +84,8 @@ __constant__ const double kAtanhC[10] = {1.0 / 21, 1.0 / 19, 1.0 / 17, 1.0 / 15,
 // divergence, against CUDA's two-path log1p (~125 issue slots per warp when
 // lanes take both paths).  Error <= 3 ulp: a different rounding of the same
 // exponential variate, not a different distribution.
-__device__ __forceinline__ double exp1_from_bits53(uint64_t x) {
+template <class Coef>
+__device__ __forceinline__ double exp1_from_bits53_c(uint64_t x, const Coef& C) {
   const double y = (double)(kKeyDomain53 - x);  // exact: 1 <= y <= 2^53
   int hi = __double2hiint(y);
   const int lo = __double2loint(y);
@@ -95,21 +96,34 @@ __device__ __forceinline__ double exp1_from_bits53(uint64_t x) {
   e += big;
   const double m = __hiloint2double(hi, lo);
   const double num = m - 1.0, den = m + 1.0;
-  double r = (double)__frcp_rn((float)den);
+  float rf;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rf) : "f"((float)den));  // den in [1.7, 2.5]
+  double r = (double)rf;
   r = fma(fma(-den, r, 1.0), r, r);
   r = fma(fma(-den, r, 1.0), r, r);
   double s = num * r;
   s = fma(fma(-den, s, num), r, s);
   const double s2 = s * s;
-  // atanh series coefficients 1/(2j+1), j = 10..1, from the constant bank
-  // (DFMA takes a c[] operand: no per-coefficient register moves)
-  double p = kAtanhC[0];
+  double p = C[0];
 #pragma unroll
-  for (int j = 1; j < 10; ++j) p = fma(p, s2, kAtanhC[j]);
+  for (int j = 1; j < 10; ++j) p = fma(p, s2, C[j]);
   const double logm = fma(2.0 * s * s2, p, 2.0 * s);
   constexpr double kLn2Hi = 6.93147180369123816490e-01, kLn2Lo = 1.90821492927058770002e-10;
   const double k = (double)(53 - e);  // E = (53 - e) ln2 - log(m)
   return fma(k, kLn2Hi, fma(k, kLn2Lo, -logm));
+}
+
+__device__ __forceinline__ double exp1_from_bits53(uint64_t x) { return exp1_from_bits53_c(x, kAtanhC); }
+
+// the atanh coefficients as kernel-parameter (constant bank 0) operands
+struct AtanhCoef {
+  double c[10];
+  __device__ __forceinline__ double operator[](int j) const { return c[j]; }
+};
+inline AtanhCoef make_atanh_coef() {
+  AtanhCoef a;
+  for (int j = 0; j < 10; ++j) a.c[j] = 1.0 / (double)(21 - 2 * j);
+  return a;
 }
 
 // --------------------------------------------------------- service in key space

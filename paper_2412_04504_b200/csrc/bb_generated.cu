@@ -147,9 +147,9 @@ struct Rep {
 
 // One request folded into its bin; closes the batch at B members
 // (on_arrival + form_batch + dispatch, simulator.hpp:187-267, one server).
-template <int SVC>
+template <int SVC, bool track>
 __device__ __forceinline__ void fold(Rep& R, uint64_t* __restrict__ slot, double* __restrict__ osum,
-                                     bool track, uint64_t xs, uint32_t B, const SvcParams& svc) {
+ uint64_t xs, uint32_t B, const SvcParams& svc) {
   const uint64_t s0 = *slot;
   const uint64_t km = max(s0 & ~kCntMask, xs << kCntBits);
   const uint32_t cnt = (uint32_t)(s0 & kCntMask) + 1;
@@ -167,8 +167,8 @@ __device__ __forceinline__ void fold(Rep& R, uint64_t* __restrict__ slot, double
   }
 }
 
-template <int SVC, int ERR, bool OVL>
-__global__ void __launch_bounds__(kGenThreads) gen_kernel(GenLaunch L) {
+template <int SVC, int ERR, bool OVL, bool TRACK>
+__global__ void __launch_bounds__(kGenThreads) gen_kernel(const __grid_constant__ GenLaunch L) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ uint64_t s_thr[kGenWarps][BB_MAX_BINS + 1];
   __shared__ __align__(16) uint8_t s_lut[kGenWarps][256];
@@ -247,12 +247,12 @@ __global__ void __launch_bounds__(kGenThreads) gen_kernel(GenLaunch L) {
       if (!OVL) {
         // ------------------------------------------------ finite arrival rate
         const double inv_lambda = P.inv_lambda;
-        const bool track = !flush;
+        constexpr bool track = TRACK;  // no flush at a finite rate: leftover sums needed
         if (track)
           for (uint32_t b = 0; b < k; ++b) s_osum[b * kGenThreads + tid] = 0.0;
         Rep R{0.0, 0.0, 0.0, 0.0, 0.0, 0};
         uint32_t cyc0 = 0;
-        const double a0 = exp1_from_bits53(draw<SVC>(cyc_rank, nt, 0, c2, c3, cyc0).xg) * inv_lambda;
+        const double a0 = exp1_from_bits53_c(draw<SVC>(cyc_rank, nt, 0, c2, c3, cyc0).xg, L.coef) * inv_lambda;
         // two requests per iteration: both draws, exponentials and bins are
         // independent, so their latencies overlap; the folds stay in order
         uint32_t i = 0;
@@ -261,8 +261,8 @@ __global__ void __launch_bounds__(kGenThreads) gen_kernel(GenLaunch L) {
           const Draw d1 = draw<SVC>(cyc_rank, nt, i + 1, c2, c3, cyc);
           uint64_t e0 = 0, e1 = 0;
           err_pair(i, e0, e1);
-          const double g0 = exp1_from_bits53(d0.xg) * inv_lambda;
-          const double g1 = exp1_from_bits53(d1.xg) * inv_lambda;
+          const double g0 = exp1_from_bits53_c(d0.xg, L.coef) * inv_lambda;
+          const double g1 = exp1_from_bits53_c(d1.xg, L.coef) * inv_lambda;
           if (out_of_support(d0.xs) || out_of_support(d1.xs)) {
             const uint32_t bad = out_of_support(d0.xs) ? i : i + 1;
             raise_error(L.err, bad, BB_EDOMAIN,
@@ -273,12 +273,12 @@ __global__ void __launch_bounds__(kGenThreads) gen_kernel(GenLaunch L) {
           const uint32_t p0 = bin_pred(d0.xs, e0), p1 = bin_pred(d1.xs, e1);
           R.t += g0;  // exponential inter-arrival, simulator.hpp:181
           R.asum += R.t;
-          fold<SVC>(R, st + (p0 - 1) * kGenThreads + tid, s_osum + (p0 - 1) * kGenThreads + tid,
-                    track, d0.xs, B, svc);
+          fold<SVC, TRACK>(R, st + (p0 - 1) * kGenThreads + tid, s_osum + (p0 - 1) * kGenThreads + tid,
+                    d0.xs, B, svc);
           R.t += g1;
           R.asum += R.t;
-          fold<SVC>(R, st + (p1 - 1) * kGenThreads + tid, s_osum + (p1 - 1) * kGenThreads + tid,
-                    track, d1.xs, B, svc);
+          fold<SVC, TRACK>(R, st + (p1 - 1) * kGenThreads + tid, s_osum + (p1 - 1) * kGenThreads + tid,
+                    d1.xs, B, svc);
         }
         if (!failed && i < n) {
           const Draw d0 = draw<SVC>(cyc_rank, nt, i, c2, c3, cyc);
@@ -289,10 +289,10 @@ __global__ void __launch_bounds__(kGenThreads) gen_kernel(GenLaunch L) {
             failed = true;
           } else {
             const uint32_t p0 = bin_pred(d0.xs, e0);
-            R.t += exp1_from_bits53(d0.xg) * inv_lambda;
+            R.t += exp1_from_bits53_c(d0.xg, L.coef) * inv_lambda;
             R.asum += R.t;
-            fold<SVC>(R, st + (p0 - 1) * kGenThreads + tid, s_osum + (p0 - 1) * kGenThreads + tid,
-                      track, d0.xs, B, svc);
+            fold<SVC, TRACK>(R, st + (p0 - 1) * kGenThreads + tid, s_osum + (p0 - 1) * kGenThreads + tid,
+                      d0.xs, B, svc);
           }
         }
         double leftover = 0.0;
@@ -458,11 +458,11 @@ __global__ void point_reduce_kernel(const double* __restrict__ rep, uint32_t n_p
 }
 
 
-template <int SVC, int ERR, bool OVL>
+template <int SVC, int ERR, bool OVL, bool TRACK>
 cudaError_t launch_gen(const GenLaunch& L, cudaStream_t s) {
   const size_t per = OVL ? (8 + 16) : 16;  // packed state + open sums | overload tables
   const size_t smem = (size_t)L.k_max * kGenThreads * per;
-  auto kern = gen_kernel<SVC, ERR, OVL>;
+  auto kern = gen_kernel<SVC, ERR, OVL, TRACK>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 0, occ = 0;
@@ -482,13 +482,18 @@ cudaError_t launch_gen(const GenLaunch& L, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+template <int SVC, int ERR>
+cudaError_t launch_mode(const GenLaunch& L, cudaStream_t s) {
+  if (L.overload) return launch_gen<SVC, ERR, true, false>(L, s);
+  return L.track ? launch_gen<SVC, ERR, false, true>(L, s) : launch_gen<SVC, ERR, false, false>(L, s);
+}
+
 template <int SVC>
 cudaError_t launch_svc(const GenLaunch& L, cudaStream_t s) {
-  const bool o = L.overload != 0;
   switch (L.err_kind) {
-    case 0: return o ? launch_gen<SVC, 0, true>(L, s) : launch_gen<SVC, 0, false>(L, s);
-    case 1: return o ? launch_gen<SVC, 1, true>(L, s) : launch_gen<SVC, 1, false>(L, s);
-    case 2: return o ? launch_gen<SVC, 2, true>(L, s) : launch_gen<SVC, 2, false>(L, s);
+    case 0: return launch_mode<SVC, 0>(L, s);
+    case 1: return launch_mode<SVC, 1>(L, s);
+    case 2: return launch_mode<SVC, 2>(L, s);
   }
   return cudaErrorInvalidValue;
 }
@@ -502,7 +507,9 @@ cudaError_t gen_setup_thresholds(GenPoint* pts_dev, uint32_t n_points, cudaStrea
   return cudaGetLastError();
 }
 
-cudaError_t gen_run(const GenLaunch& L, cudaStream_t s) {
+cudaError_t gen_run(const GenLaunch& L0, cudaStream_t s) {
+  GenLaunch L = L0;
+  L.coef = make_atanh_coef();
   switch (L.svc_kind) {
     case kSvcUniform: return launch_svc<kSvcUniform>(L, s);
     case kSvcLinear: return launch_svc<kSvcLinear>(L, s);

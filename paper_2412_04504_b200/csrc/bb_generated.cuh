@@ -39,7 +39,9 @@ struct GenLaunch {
   int32_t cyclic;
   int32_t svc_kind;          // SvcKind of every point in this launch
   int32_t overload;
+  int32_t track;             // finite rate without flush: track open arrival sums
   double* out;              // [BB_REP_FIELDS][n_points*reps_total]
+  AtanhCoef coef;           // exponential-variate polynomial (param space)
   DevError* err;
 };
 

@@ -936,11 +936,12 @@ void launch_sweep(const SweepParams* E, Sweep& W, uint64_t rep_begin, uint64_t r
   // group points by kernel instantiation; each group's points are copied
   // (already threshold-resolved) into a contiguous device array
   struct Key {
-    int err, cyc, ovl;
+    int err, cyc, ovl, track;
   };
   std::vector<Key> keys(P);
   for (size_t i = 0; i < P; ++i)
-    keys[i] = Key{(int)W.gp[i].err_kind, (int)W.gp[i].svc.kind, W.gp[i].inv_lambda == 0.0};
+    keys[i] = Key{(int)W.gp[i].err_kind, (int)W.gp[i].svc.kind, W.gp[i].inv_lambda == 0.0,
+                  W.gp[i].inv_lambda != 0.0 && !W.gp[i].flush};
   std::vector<bool> done(P, false);
   bool first = true;
   for (size_t i = 0; i < P; ++i) {
@@ -949,7 +950,7 @@ void launch_sweep(const SweepParams* E, Sweep& W, uint64_t rep_begin, uint64_t r
     uint32_t kmax = 1;
     for (size_t j = i; j < P; ++j)
       if (!done[j] && keys[j].err == keys[i].err && keys[j].cyc == keys[i].cyc &&
-          keys[j].ovl == keys[i].ovl) {
+          keys[j].ovl == keys[i].ovl && keys[j].track == keys[i].track) {
         members.push_back((uint32_t)j);
         done[j] = true;
         kmax = std::max(kmax, W.gp[j].k);
@@ -979,6 +980,7 @@ void launch_sweep(const SweepParams* E, Sweep& W, uint64_t rep_begin, uint64_t r
     L.err_kind = keys[i].err;
     L.cyclic = keys[i].cyc == bb::kSvcCyclic;
     L.svc_kind = keys[i].cyc;
+    L.track = keys[i].track;
     L.overload = keys[i].ovl;
     L.out = rep_dev;
     DBuf err(sizeof(bb::DevError), st);

@@ -517,13 +517,16 @@ struct LArgs {
   const double* R;
   const double* S;
   uint32_t nb;
-  uint8_t* split;
+  uint8_t* split;   // 1 = certified idle start, 2 = ambiguous, 0 = certified busy
+  double* Dt;       // approximate D after each batch (binade prediction)
   double* busy_part;
   double *aggA, *aggC, *incA, *incC;
   uint32_t* flag;
   uint32_t* counter;
   double tol_rel;
 };
+
+enum : uint8_t { kBusy = 0, kSplit = 1, kAmbiguous = 2 };
 
 struct MP {  // f(x) = max(x + A, C)
   double A, C;
@@ -626,11 +629,16 @@ __global__ void __launch_bounds__(LB) lindley_scan_kernel(LArgs L) {
 #pragma unroll
   for (int i = 0; i < LI; ++i) {
     if (d0 + i < L.nb) {
-      bool sp;
-      if (Dp == -CUDART_INF) sp = true;
-      else sp = R[i] > Dp + L.tol_rel * fmax(fabs(Dp), fabs(R[i]));
-      L.split[d0 + i] = sp;
+      uint8_t code;
+      if (Dp == -CUDART_INF) {
+        code = kSplit;
+      } else {
+        const double tol = L.tol_rel * fmax(fabs(Dp), fabs(R[i]));
+        code = R[i] > Dp + tol ? kSplit : (R[i] >= Dp - tol ? kAmbiguous : kBusy);
+      }
+      L.split[d0 + i] = code;
       Dp = fmax(Dp, R[i]) + S[i];
+      L.Dt[d0 + i] = Dp;
     }
   }
 }
@@ -638,9 +646,11 @@ __global__ void __launch_bounds__(LB) lindley_scan_kernel(LArgs L) {
 // Exact serial recurrence inside every certified busy period.
 __global__ void lindley_segments_kernel(const double* __restrict__ R, const double* __restrict__ S,
                                         const uint8_t* __restrict__ split, uint32_t nb,
-                                        double* __restrict__ start, double* __restrict__ finish) {
+                                        double* __restrict__ start, double* __restrict__ finish,
+                                        const int* __restrict__ bad) {
+  if (!*bad) return;  // fallback only: the binade scan produced exact values
   const uint32_t d = blockIdx.x * blockDim.x + threadIdx.x;
-  if (d >= nb || !split[d]) return;
+  if (d >= nb || split[d] != kSplit) return;
   double D = __dadd_rn(R[d], S[d]);  // idle server: start = formation time
   start[d] = R[d];
   finish[d] = D;
@@ -651,7 +661,7 @@ __global__ void lindley_segments_kernel(const double* __restrict__ R, const doub
 #pragma unroll
     for (int i = 0; i < CH; ++i) {
       const bool v = e0 + i < nb;
-      sp[i] = v ? split[e0 + i] : 1;
+      sp[i] = v ? split[e0 + i] == kSplit : 1;
       r[i] = v ? R[e0 + i] : 0.0;
       s[i] = v ? S[e0 + i] : 0.0;
     }
@@ -664,6 +674,251 @@ __global__ void lindley_segments_kernel(const double* __restrict__ R, const doub
       finish[e0 + i] = D;
     }
   }
+}
+
+// ----------------------------------------------------- exact parallel Lindley
+// Inside a busy period D_d = fl(D_{d-1} + S_d).  While D stays in one binade
+// [2^E, 2^(E+1)) every value is a multiple of u = 2^(E-52): D = a*u with the
+// integer a in [2^52, 2^53), and round-to-nearest-even of a*u + S is
+//     a + q + [f > 1/2] + [f == 1/2 and (a + q) odd],   S/u = q + f,
+// an increment that depends on a only through its parity.  Such maps
+// (inc for even a, inc for odd a) compose associatively, so a segmented scan
+// evaluates the sequential fp64 chain exactly.  Runs of one binade are cut at
+// certified idle starts, ambiguous reset points and predicted binade
+// crossings ("heads"); one thread per busy period then walks its few heads
+// (exact fp64 steps), and every other batch reads its value from its run's
+// head and its prefix map.  Any violated assumption (a prediction off by a
+// binade) raises a flag and the host falls back to the serial kernel.
+struct PMap {
+  long long i0, i1;  // increment for even / odd starting integer
+};
+__device__ __forceinline__ PMap pcompose(const PMap& x, const PMap& y) {  // y after x
+  return PMap{x.i0 + ((x.i0 & 1) ? y.i1 : y.i0), x.i1 + ((x.i1 & 1) ? y.i0 : y.i1)};
+}
+__device__ __forceinline__ int binade(double v) { return (int)((__double_as_longlong(v) >> 52) & 0x7FF) - 1023; }
+
+// Is batch d a run head?  (needs d's code and the approximate D before/after)
+__device__ __forceinline__ bool run_head(uint8_t code, double dprev, double dcur, double tol_rel) {
+  if (code != kBusy) return true;
+  if (!(dprev > 0.0) || !(dcur > 0.0)) return true;
+  const int e = binade(dcur);
+  if (binade(dprev) != e) return true;
+  const double lo = ldexp(1.0, e), hi = ldexp(1.0, e + 1);
+  return dprev < lo * (1.0 + 4 * tol_rel) || dcur > hi * (1.0 - 4 * tol_rel);
+}
+
+// map of one batch in binade e (q = floor(S/u), f = S/u - q exact)
+__device__ __forceinline__ PMap batch_map(double S, int e) {
+  const double x = ldexp(S, 52 - e);
+  const double qd = floor(x);
+  const double f = x - qd;
+  const long long q = (long long)qd;
+  const long long up = f > 0.5;
+  const long long half = f == 0.5;
+  // a + q + 0.5 with (a+q) odd rounds up; even a: parity of q decides
+  return PMap{q + up + (half & (q & 1)), q + up + (half & ((q + 1) & 1))};
+}
+
+struct BArgs {
+  const double* R;
+  const double* S;
+  const double* Dt;
+  const uint8_t* code;
+  uint32_t nb;
+  double tol_rel;
+  long long* p0;       // prefix map per batch (within its run)
+  long long* p1;
+  uint32_t* head_of;   // run head of each batch
+  uint32_t* run_last;  // last batch of each run, indexed by head
+  // look-back
+  long long *ag0, *ag1, *in0, *in1;
+  uint32_t *agh, *inh, *agf, *inf;  // head position (+1, 0 = none) and head flag
+  uint32_t* flag;
+  uint32_t* counter;
+};
+
+struct SegV {
+  PMap m;
+  uint32_t hp;   // 1 + index of the latest head (0 = none)
+  uint32_t hf;   // contains a head
+};
+__device__ __forceinline__ SegV scomb(const SegV& x, const SegV& y) {  // y after x
+  SegV r;
+  r.m = y.hf ? y.m : pcompose(x.m, y.m);
+  r.hp = y.hp > x.hp ? y.hp : x.hp;
+  r.hf = x.hf | y.hf;
+  return r;
+}
+
+__global__ void __launch_bounds__(LB) binade_scan_kernel(BArgs A) {
+  __shared__ SegV s_w[LB / 32];
+  __shared__ SegV s_pre;
+  __shared__ uint32_t s_blk;
+  const uint32_t tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  if (tid == 0) s_blk = atomicAdd(A.counter, 1u);
+  __syncthreads();
+  const uint32_t blk = s_blk;
+  const uint64_t d0 = (uint64_t)blk * LTILE + tid * LI;
+  SegV v[LI];
+  SegV acc{{0, 0}, 0, 0};
+#pragma unroll
+  for (int i = 0; i < LI; ++i) {
+    const uint64_t d = d0 + i;
+    SegV e{{0, 0}, 0, 0};
+    if (d < A.nb) {
+      const double dcur = A.Dt[d];
+      const double dprev = d ? A.Dt[d - 1] : -1.0;
+      if (run_head(A.code[d], dprev, dcur, A.tol_rel)) {
+        e.hf = 1;
+        e.hp = (uint32_t)d + 1;
+      } else {
+        e.m = batch_map(A.S[d], binade(dcur));
+      }
+    }
+    acc = scomb(acc, e);
+    v[i] = acc;
+  }
+  SegV x = acc;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    SegV y;
+    y.m.i0 = __shfl_up_sync(0xffffffffu, x.m.i0, o);
+    y.m.i1 = __shfl_up_sync(0xffffffffu, x.m.i1, o);
+    y.hp = __shfl_up_sync(0xffffffffu, x.hp, o);
+    y.hf = __shfl_up_sync(0xffffffffu, x.hf, o);
+    if (lane >= o) x = scomb(y, x);
+  }
+  if (lane == 31) s_w[w] = x;
+  __syncthreads();
+  if (tid == 0) {
+    SegV agg{{0, 0}, 0, 0};
+    for (int q = 0; q < LB / 32; ++q) agg = scomb(agg, s_w[q]);
+    SegV pre{{0, 0}, 0, 0};
+    if (blk == 0) {
+      A.in0[0] = agg.m.i0; A.in1[0] = agg.m.i1; A.inh[0] = agg.hp; A.inf[0] = agg.hf;
+      __threadfence();
+      st_release32(&A.flag[0], 2);
+    } else {
+      A.ag0[blk] = agg.m.i0; A.ag1[blk] = agg.m.i1; A.agh[blk] = agg.hp; A.agf[blk] = agg.hf;
+      __threadfence();
+      st_release32(&A.flag[blk], 1);
+      SegV run{{0, 0}, 0, 0};
+      int64_t p = (int64_t)blk - 1;
+      while (true) {
+        uint32_t fl;
+        do {
+          fl = ld_acquire32(&A.flag[p]);
+        } while (fl == 0);
+        SegV t;
+        if (fl == 2) {
+          t.m.i0 = *(volatile long long*)&A.in0[p]; t.m.i1 = *(volatile long long*)&A.in1[p];
+          t.hp = *(volatile uint32_t*)&A.inh[p]; t.hf = *(volatile uint32_t*)&A.inf[p];
+          run = scomb(t, run);
+          break;
+        }
+        t.m.i0 = *(volatile long long*)&A.ag0[p]; t.m.i1 = *(volatile long long*)&A.ag1[p];
+        t.hp = *(volatile uint32_t*)&A.agh[p]; t.hf = *(volatile uint32_t*)&A.agf[p];
+        run = scomb(t, run);
+        if (run.hf) break;  // a head resets the map; the head position is the max seen
+        --p;
+      }
+      pre = run;
+      const SegV inc = scomb(pre, agg);
+      A.in0[blk] = inc.m.i0; A.in1[blk] = inc.m.i1; A.inh[blk] = inc.hp; A.inf[blk] = inc.hf;
+      __threadfence();
+      st_release32(&A.flag[blk], 2);
+    }
+    s_pre = pre;
+  }
+  __syncthreads();
+  SegV pre = s_pre;
+  for (uint32_t q = 0; q < w; ++q) pre = scomb(pre, s_w[q]);
+  SegV xl;
+  xl.m.i0 = __shfl_up_sync(0xffffffffu, x.m.i0, 1);
+  xl.m.i1 = __shfl_up_sync(0xffffffffu, x.m.i1, 1);
+  xl.hp = __shfl_up_sync(0xffffffffu, x.hp, 1);
+  xl.hf = __shfl_up_sync(0xffffffffu, x.hf, 1);
+  if (lane > 0) pre = scomb(pre, xl);
+#pragma unroll
+  for (int i = 0; i < LI; ++i) {
+    const uint64_t d = d0 + i;
+    if (d >= A.nb) break;
+    const SegV r = scomb(pre, v[i]);
+    A.p0[d] = r.m.i0;
+    A.p1[d] = r.m.i1;
+    const uint32_t h = r.hp - 1;  // batch 0 is always a head
+    A.head_of[d] = h;
+    bool last = d + 1 == A.nb;
+    if (!last) last = run_head(A.code[d + 1], A.Dt[d], A.Dt[d + 1], A.tol_rel);
+    if (last) A.run_last[h] = (uint32_t)d;
+  }
+}
+
+// value of the run's last batch from its head value (exact), or a fallback flag
+__device__ __forceinline__ double run_end(double Dh, uint32_t h, uint32_t last, const double* Dt,
+                                          const long long* p0, const long long* p1, int* bad) {
+  if (last == h) return Dh;
+  const int e = binade(Dt[last]);
+  if (binade(Dh) != e) {
+    *bad = 1;
+    return Dh;
+  }
+  const long long a = (long long)ldexp(Dh, 52 - e);
+  const long long al = a + ((a & 1) ? p1[last] : p0[last]);
+  if (al > (1ll << 53)) *bad = 1;
+  return ldexp((double)al, e - 52);
+}
+
+// one thread per busy period: walk its run heads (exact fp64 steps)
+__global__ void binade_chain_kernel(const double* __restrict__ R, const double* __restrict__ S,
+                                    const double* __restrict__ Dt, const uint8_t* __restrict__ code,
+                                    const long long* __restrict__ p0, const long long* __restrict__ p1,
+                                    const uint32_t* __restrict__ run_last, uint32_t nb,
+                                    double* __restrict__ start, double* __restrict__ finish,
+                                    int* bad) {
+  const uint32_t d = blockIdx.x * blockDim.x + threadIdx.x;
+  if (d >= nb || code[d] != kSplit) return;
+  uint32_t h = d;
+  double D = __dadd_rn(R[h], S[h]);  // idle server: start = formation time
+  start[h] = R[h];
+  finish[h] = D;
+  while (true) {
+    const uint32_t last = run_last[h];
+    D = run_end(D, h, last, Dt, p0, p1, bad);
+    const uint32_t nx = last + 1;
+    if (nx >= nb || code[nx] == kSplit) return;
+    h = nx;
+    const double st = fmax(D, R[h]);  // ambiguous reset or binade crossing: exact step
+    D = __dadd_rn(st, S[h]);
+    start[h] = st;
+    finish[h] = D;
+  }
+}
+
+// every non-head batch: value from its run head and prefix map
+__global__ void binade_fill_kernel(const double* __restrict__ S, const double* __restrict__ Dt,
+                                   const uint8_t* __restrict__ code, const long long* __restrict__ p0,
+                                   const long long* __restrict__ p1, const uint32_t* __restrict__ head_of,
+                                   uint32_t nb, double tol_rel, double* __restrict__ start,
+                                   double* __restrict__ finish, int* bad) {
+  const uint32_t d = blockIdx.x * blockDim.x + threadIdx.x;
+  if (d >= nb) return;
+  const double dprev = d ? Dt[d - 1] : -1.0;
+  if (run_head(code[d], dprev, Dt[d], tol_rel)) return;
+  const uint32_t h = head_of[d];
+  const double Dh = finish[h];
+  const int e = binade(Dt[d]);
+  if (binade(Dh) != e) {
+    *bad = 1;
+    return;
+  }
+  const long long a = (long long)ldexp(Dh, 52 - e);
+  const long long ap = (d - 1 == h) ? a : a + ((a & 1) ? p1[d - 1] : p0[d - 1]);
+  const long long ad = a + ((a & 1) ? p1[d] : p0[d]);
+  const long long q = (long long)floor(ldexp(S[d], 52 - e));
+  if (ap + q >= (1ll << 53) || ad > (1ll << 53) || ap < (1ll << 52)) *bad = 1;
+  start[d] = ldexp((double)ap, e - 52);
+  finish[d] = ldexp((double)ad, e - 52);
 }
 
 // ------------------------------------------------------------- requests
@@ -1020,16 +1275,58 @@ void trace_run(const TraceArgs& A, TraceResult* R, cudaStream_t s) {
     BB_CK(pool.alloc((void**)&busy_sum, 8));
     BB_CK(pool.alloc((void**)&lflag, (size_t)lt * 4));
     BB_CK(cudaMemsetAsync(lflag, 0, (size_t)lt * 4, s));
+    const double tol_rel = (double)(nb + 4096) * 0x1.0p-50;
+    double* Dt;
+    BB_CK(pool.alloc((void**)&Dt, (size_t)nb * 8 + 8));
     {
-      LArgs L{dR, dS, nb, split, busy_part, aggA, aggC, incA, incC, lflag, ws.counters + 1,
-              (double)(nb + 4096) * 0x1.0p-50};
+      LArgs L{dR, dS, nb, split, Dt, busy_part, aggA, aggC, incA, incC, lflag, ws.counters + 1,
+              tol_rel};
       if (nb) lindley_scan_kernel<<<lt, LB, 0, s>>>(L);
       note_launch();
       BB_CK(cudaGetLastError());
     }
-    if (nb) lindley_segments_kernel<<<grid_for(nb, 128), 128, 0, s>>>(dR, dS, split, nb, start, finish);
-    note_launch();
-    BB_CK(cudaGetLastError());
+    // exact values: binade parity scan (parallel), serial segments only as a fallback
+    int* bad;
+    BB_CK(pool.alloc((void**)&bad, 4));
+    BB_CK(cudaMemsetAsync(bad, 0, 4, s));
+    if (nb) {
+      BArgs Bq{};
+      Bq.R = dR;
+      Bq.S = dS;
+      Bq.Dt = Dt;
+      Bq.code = split;
+      Bq.nb = nb;
+      Bq.tol_rel = tol_rel;
+      BB_CK(pool.alloc((void**)&Bq.p0, (size_t)nb * 8));
+      BB_CK(pool.alloc((void**)&Bq.p1, (size_t)nb * 8));
+      BB_CK(pool.alloc((void**)&Bq.head_of, (size_t)nb * 4));
+      BB_CK(pool.alloc((void**)&Bq.run_last, (size_t)nb * 4));
+      BB_CK(pool.alloc((void**)&Bq.ag0, (size_t)lt * 8));
+      BB_CK(pool.alloc((void**)&Bq.ag1, (size_t)lt * 8));
+      BB_CK(pool.alloc((void**)&Bq.in0, (size_t)lt * 8));
+      BB_CK(pool.alloc((void**)&Bq.in1, (size_t)lt * 8));
+      BB_CK(pool.alloc((void**)&Bq.agh, (size_t)lt * 4));
+      BB_CK(pool.alloc((void**)&Bq.inh, (size_t)lt * 4));
+      BB_CK(pool.alloc((void**)&Bq.agf, (size_t)lt * 4));
+      BB_CK(pool.alloc((void**)&Bq.inf, (size_t)lt * 4));
+      BB_CK(pool.alloc((void**)&Bq.flag, (size_t)lt * 4));
+      BB_CK(cudaMemsetAsync(Bq.flag, 0, (size_t)lt * 4, s));
+      Bq.counter = ws.counters + 2;
+      binade_scan_kernel<<<lt, LB, 0, s>>>(Bq);
+      note_launch();
+      BB_CK(cudaGetLastError());
+      binade_chain_kernel<<<grid_for(nb, 128), 128, 0, s>>>(dR, dS, Dt, split, Bq.p0, Bq.p1,
+                                                            Bq.run_last, nb, start, finish, bad);
+      note_launch();
+      BB_CK(cudaGetLastError());
+      binade_fill_kernel<<<grid_for(nb, 256), 256, 0, s>>>(dS, Dt, split, Bq.p0, Bq.p1, Bq.head_of,
+                                                           nb, tol_rel, start, finish, bad);
+      note_launch();
+      BB_CK(cudaGetLastError());
+      lindley_segments_kernel<<<grid_for(nb, 128), 128, 0, s>>>(dR, dS, split, nb, start, finish, bad);
+      note_launch();
+      BB_CK(cudaGetLastError());
+    }
     sum_kernel<<<1, 256, 0, s>>>(busy_part, nb ? lt : 0, busy_sum);
     note_launch();
     BB_CK(cudaGetLastError());
