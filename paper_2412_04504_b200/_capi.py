@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libbinbatch_b200.so")
+LIB_PATH = os.environ.get("BB_LIB_PATH") or os.path.join(PKG, "libbinbatch_b200.so")
 
 BB_OK, BB_EINVAL, BB_EDOMAIN, BB_ERUNTIME, BB_ECUDA, BB_EUNSUPPORTED = range(6)
 BB_MAX_BINS = 64

@@ -18,8 +18,10 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-OUT = os.path.join(PKG, "_build")
-LIB = os.path.join(PKG, "libbinbatch_b200.so")
+OUT = os.path.join(PKG, "_build" + os.environ.get("BB_BUILD_SUFFIX", ""))
+LIB = os.path.join(PKG, os.environ.get("BB_LIB_NAME", "libbinbatch_b200.so"))
+# experiment variants: BB_DEFINES="-DBB_GEN_MINB=4" BB_LIB_NAME=libvariant.so
+EXTRA = os.environ.get("BB_DEFINES", "").split()
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -42,7 +44,7 @@ def _compile(src: str, verbose: bool) -> str:
     newest = max([os.path.getmtime(src)] + [os.path.getmtime(h) for h in _headers()])
     if os.path.exists(obj) and os.path.getmtime(obj) >= newest:
         return obj
-    cmd = [NVCC] + COMMON + PER_FILE.get(os.path.basename(src), [])
+    cmd = [NVCC] + COMMON + EXTRA + PER_FILE.get(os.path.basename(src), [])
     if src.endswith(".cpp"):
         cmd += ["-x", "cu"]
     cmd += ["-c", src, "-o", obj]

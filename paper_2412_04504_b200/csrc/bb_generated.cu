@@ -167,8 +167,14 @@ __device__ __forceinline__ void fold(Rep& R, uint64_t* __restrict__ slot, double
   }
 }
 
+#ifndef BB_GEN_MINB
+#define BB_GEN_MINB 1
+#endif
+#ifndef BB_GEN_UNROLL
+#define BB_GEN_UNROLL 4  // requests in flight per thread (even)
+#endif
 template <int SVC, int ERR, bool OVL, bool TRACK>
-__global__ void __launch_bounds__(kGenThreads) gen_kernel(const __grid_constant__ GenLaunch L) {
+__global__ void __launch_bounds__(kGenThreads, BB_GEN_MINB) gen_kernel(const __grid_constant__ GenLaunch L) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ uint64_t s_thr[kGenWarps][BB_MAX_BINS + 1];
   __shared__ __align__(16) uint8_t s_lut[kGenWarps][256];
@@ -253,37 +259,53 @@ __global__ void __launch_bounds__(kGenThreads) gen_kernel(const __grid_constant_
         Rep R{0.0, 0.0, 0.0, 0.0, 0.0, 0};
         uint32_t cyc0 = 0;
         const double a0 = exp1_from_bits53_c(draw<SVC>(cyc_rank, nt, 0, c2, c3, cyc0).xg, L.coef) * inv_lambda;
-        // two requests per iteration: both draws, exponentials and bins are
-        // independent, so their latencies overlap; the folds stay in order
+        // U requests per iteration: their draws, exponentials and bins are
+        // independent, so the latencies overlap; the folds stay in order
+        constexpr int U = BB_GEN_UNROLL;
         uint32_t i = 0;
-        for (; i + 2 <= n; i += 2) {
-          const Draw d0 = draw<SVC>(cyc_rank, nt, i, c2, c3, cyc);
-          const Draw d1 = draw<SVC>(cyc_rank, nt, i + 1, c2, c3, cyc);
-          uint64_t e0 = 0, e1 = 0;
-          err_pair(i, e0, e1);
-          const double g0 = exp1_from_bits53_c(d0.xg, L.coef) * inv_lambda;
-          const double g1 = exp1_from_bits53_c(d1.xg, L.coef) * inv_lambda;
-          if (out_of_support(d0.xs) || out_of_support(d1.xs)) {
-            const uint32_t bad = out_of_support(d0.xs) ? i : i + 1;
-            raise_error(L.err, bad, BB_EDOMAIN,
-                        svc_of_key_t<SVC>(svc, bad == i ? d0.xs : d1.xs), r);
+        for (; i + U <= n; i += U) {
+          Draw d[U];
+          uint64_t e[U];
+          double g[U];
+          uint32_t pb[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) d[u] = draw<SVC>(cyc_rank, nt, i + u, c2, c3, cyc);
+#pragma unroll
+          for (int u = 0; u < U; u += 2) {
+            e[u] = e[u + 1] = 0;
+            err_pair(i + u, e[u], e[u + 1]);
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u) g[u] = exp1_from_bits53_c(d[u].xg, L.coef) * inv_lambda;
+          bool oos = false;
+#pragma unroll
+          for (int u = 0; u < U; ++u) oos |= out_of_support(d[u].xs);
+          if (oos) {  // first offending request (no dynamic indexing: keeps d[] in registers)
+            uint32_t bad = 0;
+            uint64_t bx = 0;
+#pragma unroll
+            for (int u = U - 1; u >= 0; --u)
+              if (out_of_support(d[u].xs)) bad = (uint32_t)u, bx = d[u].xs;
+            raise_error(L.err, i + bad, BB_EDOMAIN, svc_of_key_t<SVC>(svc, bx), r);
             failed = true;
             break;
           }
-          const uint32_t p0 = bin_pred(d0.xs, e0), p1 = bin_pred(d1.xs, e1);
-          R.t += g0;  // exponential inter-arrival, simulator.hpp:181
-          R.asum += R.t;
-          fold<SVC, TRACK>(R, st + (p0 - 1) * kGenThreads + tid, s_osum + (p0 - 1) * kGenThreads + tid,
-                    d0.xs, B, svc);
-          R.t += g1;
-          R.asum += R.t;
-          fold<SVC, TRACK>(R, st + (p1 - 1) * kGenThreads + tid, s_osum + (p1 - 1) * kGenThreads + tid,
-                    d1.xs, B, svc);
+#pragma unroll
+          for (int u = 0; u < U; ++u) pb[u] = bin_pred(d[u].xs, e[u]);
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            R.t += g[u];  // exponential inter-arrival, simulator.hpp:181
+            R.asum += R.t;
+            fold<SVC, TRACK>(R, st + (pb[u] - 1) * kGenThreads + tid,
+                             s_osum + (pb[u] - 1) * kGenThreads + tid, d[u].xs, B, svc);
+          }
         }
-        if (!failed && i < n) {
+        // tail: fewer than U requests left, one at a time
+        for (; !failed && i < n; ++i) {
           const Draw d0 = draw<SVC>(cyc_rank, nt, i, c2, c3, cyc);
           uint64_t e0 = 0, e1 = 0;
-          err_pair(i, e0, e1);
+          err_pair(i & ~1u, e0, e1);
+          if (i & 1u) e0 = e1;
           if (out_of_support(d0.xs)) {
             raise_error(L.err, i, BB_EDOMAIN, svc_of_key_t<SVC>(svc, d0.xs), r);
             failed = true;
@@ -460,7 +482,8 @@ __global__ void point_reduce_kernel(const double* __restrict__ rep, uint32_t n_p
 
 template <int SVC, int ERR, bool OVL, bool TRACK>
 cudaError_t launch_gen(const GenLaunch& L, cudaStream_t s) {
-  const size_t per = OVL ? (8 + 16) : 16;  // packed state + open sums | overload tables
+  // packed state (+ open arrival sums without flush | + overload tables)
+  const size_t per = OVL ? (8 + 16) : (TRACK ? 16 : 8);
   const size_t smem = (size_t)L.k_max * kGenThreads * per;
   auto kern = gen_kernel<SVC, ERR, OVL, TRACK>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -73,7 +73,9 @@ struct Info {
 
 struct WS {
   uint32_t* counters;            // [0] partition tiles, [1] lindley tiles
-  unsigned long long* desc1;     // [ntiles*k] flag|count
+  uint32_t* flag1;               // [ntiles] 1 = aggregate, 2 = inclusive published
+  uint32_t* cagg;                // [ntiles*k] tile per-bin counts
+  uint32_t* cinc;                // [ntiles*k] inclusive per-bin counts
   unsigned long long* desc2v;    // [ntiles*k] alpha<<63 | open-max bits
   uint32_t* desc2f;              // [ntiles*k]
   uint8_t* pb8;
@@ -227,26 +229,48 @@ __global__ void __launch_bounds__(TB) partition_kernel(PartArgs P) {
       }
       tot = run;
       s_tot[lane] = tot;
-      // phase-1 decoupled look-back on the per-bin counts
-      unsigned long long* d = P.ws.desc1 + (uint64_t)t * k + lane;
-      if (t == 0) {
-        st_release64(d, FLAG_P | tot);
-      } else {
-        st_release64(d, FLAG_A | tot);
-        unsigned long long acc = 0;
-        int64_t p = (int64_t)t - 1;
-        while (true) {
-          unsigned long long v;
+      if (t == 0) P.ws.cinc[lane] = tot;
+      else P.ws.cagg[(uint64_t)t * k + lane] = tot;
+    }
+    // phase-1 decoupled look-back on the k-vector of counts; one flag per
+    // tile, a window of 32 predecessors per round trip (lane i: tile base-i)
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence();
+      st_release32(&P.ws.flag1[t], t == 0 ? 2u : 1u);
+    }
+    if (t > 0) {
+      int64_t base = (int64_t)t - 1;
+      uint32_t acc = 0;
+      while (true) {
+        const int64_t p = base - (int64_t)lane;
+        uint32_t f = 2;
+        if (p >= 0) {
           do {
-            v = ld_acquire64(P.ws.desc1 + (uint64_t)p * k + lane);
-          } while ((v >> 62) == 0);
-          acc += v & VAL_MASK;
-          if ((v >> 62) == 2) break;
-          --p;
+            f = ld_acquire32(&P.ws.flag1[p]);
+          } while (f == 0);
         }
-        excl = (uint32_t)acc;
-        st_release64(d, FLAG_P | (acc + tot));
+        const uint32_t incm = __ballot_sync(0xffffffffu, f == 2);
+        __syncwarp();  // the window's flags are observed before any lane reads its counts
+        const int last = incm ? __ffs(incm) - 1 : 31;
+        if (lane < k) {
+          for (int i = 0; i <= last; ++i) {
+            const uint64_t q = (uint64_t)(base - i) * k + lane;
+            acc += (incm && i == last) ? __ldcg(&P.ws.cinc[q]) : __ldcg(&P.ws.cagg[q]);
+          }
+        }
+        if (incm) break;
+        base -= 32;
       }
+      excl = acc;
+      if (lane < k) P.ws.cinc[(uint64_t)t * k + lane] = acc + tot;
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence();
+        st_release32(&P.ws.flag1[t], 2u);
+      }
+    }
+    if (lane < k) {
       const uint32_t jlo = P.divB.div(excl);
       nfrag = tot ? P.divB.div(excl + tot - 1) - jlo + 1 : 0;
       s_excl[lane] = excl;
@@ -1153,7 +1177,9 @@ void trace_run(const TraceArgs& A, TraceResult* R, cudaStream_t s) {
   BB_CK(cudaEventCreate(&ev1));
   BB_CK(cudaEventCreate(&ev2));
   BB_CK(pool.alloc((void**)&ws.counters, 16));
-  BB_CK(pool.alloc((void**)&ws.desc1, (size_t)ntiles * k * 8));
+  BB_CK(pool.alloc((void**)&ws.flag1, (size_t)ntiles * 4));
+  BB_CK(pool.alloc((void**)&ws.cagg, (size_t)ntiles * k * 4));
+  BB_CK(pool.alloc((void**)&ws.cinc, (size_t)ntiles * k * 4));
   BB_CK(pool.alloc((void**)&ws.desc2v, (size_t)ntiles * k * 8));
   BB_CK(pool.alloc((void**)&ws.desc2f, (size_t)ntiles * k * 4));
   BB_CK(pool.alloc((void**)&ws.pb8, n));
@@ -1169,7 +1195,7 @@ void trace_run(const TraceArgs& A, TraceResult* R, cudaStream_t s) {
   BB_CK(pool.alloc((void**)&ws.err, sizeof(DevError)));
   BB_CK(pool.alloc((void**)&ws.info, sizeof(Info)));
   BB_CK(cudaMemsetAsync(ws.counters, 0, 16, s));
-  BB_CK(cudaMemsetAsync(ws.desc1, 0, (size_t)ntiles * k * 8, s));
+  BB_CK(cudaMemsetAsync(ws.flag1, 0, (size_t)ntiles * 4, s));
   BB_CK(cudaMemsetAsync(ws.desc2f, 0, (size_t)ntiles * k * 4, s));
   BB_CK(cudaMemsetAsync(ws.fin_cnt, 0, 32 * 8, s));
   BB_CK(cudaMemsetAsync(ws.fin_open, 0, 32 * 8, s));
