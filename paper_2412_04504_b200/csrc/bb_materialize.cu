@@ -61,37 +61,49 @@ __global__ void __launch_bounds__(MT) scan_kernel(const double* __restrict__ g, 
   }
   if (lane == 31) s_w[w] = x;
   __syncthreads();
-  if (tid == 0) {
+  if (w == 0) {
     double agg = 0.0;
     for (int q = 0; q < MT / 32; ++q) agg += s_w[q];
-    double pre = 0.0;
-    if (blk == 0) {
-      incv[0] = agg;
+    if (lane == 0) {
+      if (blk == 0) incv[0] = agg;
+      else aggv[blk] = agg;
       __threadfence();
-      atomicExch(&flag[0], 2u);
-    } else {
-      aggv[blk] = agg;
-      __threadfence();
-      atomicExch(&flag[blk], 1u);
-      int64_t p = (int64_t)blk - 1;
-      while (true) {
-        uint32_t f;
-        do {
-          f = *(volatile uint32_t*)&flag[p];
-        } while (f == 0);
-        __threadfence();
-        if (f == 2) {
-          pre += *(volatile double*)&incv[p];
-          break;
-        }
-        pre += *(volatile double*)&aggv[p];
-        --p;
-      }
-      incv[blk] = pre + agg;
-      __threadfence();
-      atomicExch(&flag[blk], 2u);
+      atomicExch(&flag[blk], blk == 0 ? 2u : 1u);
     }
-    s_pre = pre;
+    double pre = 0.0;
+    if (blk > 0) {  // warp-cooperative look-back: 32 predecessors per round trip
+      int64_t base = (int64_t)blk - 1;
+      while (true) {
+        const int64_t p = base - (int64_t)lane;
+        uint32_t f = 2;
+        double v = 0.0;
+        if (p >= 0) {
+          do {
+            f = *(volatile uint32_t*)&flag[p];
+          } while (f == 0);
+          __threadfence();
+          v = f == 2 ? *(volatile double*)&incv[p] : *(volatile double*)&aggv[p];
+        }
+        const uint32_t incm = __ballot_sync(0xffffffffu, f == 2);
+        const uint32_t last = incm ? (uint32_t)(__ffs(incm) - 1) : 31u;
+        if (lane > last) v = 0.0;
+        // sum in tile order (earliest first), as a sequential look-back would
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const double other = __shfl_down_sync(0xffffffffu, v, o);
+          if (lane + o <= last) v = other + v;
+        }
+        pre = __shfl_sync(0xffffffffu, v, 0) + pre;
+        if (incm) break;
+        base -= 32;
+      }
+      if (lane == 0) {
+        incv[blk] = pre + agg;
+        __threadfence();
+        atomicExch(&flag[blk], 2u);
+      }
+    }
+    if (lane == 0) s_pre = pre;
   }
   __syncthreads();
   double pre = s_pre;

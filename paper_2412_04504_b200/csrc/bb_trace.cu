@@ -31,6 +31,7 @@ constexpr unsigned long long KEY_UNSERVED = ~0ull;
 constexpr uint32_t FL_NONMONO = 1, FL_TIE_GT_B = 2, FL_NOT_ALL_EQUAL = 4;
 constexpr int LB = 256, LI = 8, LTILE = LB * LI;  // Lindley scan tile
 constexpr int HBITS = 12, HBINS = 1 << HBITS;
+constexpr int kLookWin = 8;  // predecessors per look-back round trip (packed words: relaxed loads)
 
 __device__ __forceinline__ void st_release64(unsigned long long* p, unsigned long long v) {
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
@@ -73,9 +74,7 @@ struct Info {
 
 struct WS {
   uint32_t* counters;            // [0] partition tiles, [1] lindley tiles
-  uint32_t* flag1;               // [ntiles] 1 = aggregate, 2 = inclusive published
-  uint32_t* cagg;                // [ntiles*k] tile per-bin counts
-  uint32_t* cinc;                // [ntiles*k] inclusive per-bin counts
+  unsigned long long* desc1;     // [ntiles*k] flag(2 bits) | count
   unsigned long long* desc2v;    // [ntiles*k] alpha<<63 | open-max bits
   uint32_t* desc2f;              // [ntiles*k]
   uint8_t* pb8;
@@ -229,45 +228,37 @@ __global__ void __launch_bounds__(TB) partition_kernel(PartArgs P) {
       }
       tot = run;
       s_tot[lane] = tot;
-      if (t == 0) P.ws.cinc[lane] = tot;
-      else P.ws.cagg[(uint64_t)t * k + lane] = tot;
     }
-    // phase-1 decoupled look-back on the k-vector of counts; one flag per
-    // tile, a window of 32 predecessors per round trip (lane i: tile base-i)
-    __syncwarp();
-    if (lane == 0) {
-      __threadfence();
-      st_release32(&P.ws.flag1[t], t == 0 ? 2u : 1u);
-    }
-    if (t > 0) {
-      int64_t base = (int64_t)t - 1;
-      uint32_t acc = 0;
-      while (true) {
-        const int64_t p = base - (int64_t)lane;
-        uint32_t f = 2;
-        if (p >= 0) {
-          do {
-            f = ld_acquire32(&P.ws.flag1[p]);
-          } while (f == 0);
-        }
-        const uint32_t incm = __ballot_sync(0xffffffffu, f == 2);
-        __syncwarp();  // the window's flags are observed before any lane reads its counts
-        const int last = incm ? __ffs(incm) - 1 : 31;
-        if (lane < k) {
-          for (int i = 0; i <= last; ++i) {
-            const uint64_t q = (uint64_t)(base - i) * k + lane;
-            acc += (incm && i == last) ? __ldcg(&P.ws.cinc[q]) : __ldcg(&P.ws.cagg[q]);
+    // phase-1 decoupled look-back, one bin per lane: each round trip loads
+    // the packed (flag | count) words of kLookWin predecessors for the lane's bin
+    if (lane < k) {
+      unsigned long long* dsc = P.ws.desc1 + (uint64_t)t * k + lane;
+      if (t == 0) {
+        st_release64(dsc, FLAG_P | tot);
+      } else {
+        st_release64(dsc, FLAG_A | tot);
+        unsigned long long acc = 0;
+        int64_t p = (int64_t)t - 1;
+        bool done = false;
+        while (!done) {
+          unsigned long long v[kLookWin];
+#pragma unroll
+          for (int i = 0; i < kLookWin; ++i)
+            v[i] = p - i >= 0 ? ld_relaxed64(P.ws.desc1 + (uint64_t)(p - i) * k + lane) : FLAG_P;
+          int i = 0;
+          for (; i < kLookWin; ++i) {
+            const unsigned long long f = v[i] >> 62;
+            if (f == 0) break;          // not yet published: reload from here
+            acc += v[i] & VAL_MASK;
+            if (f == 2) {
+              done = true;
+              break;
+            }
           }
+          p -= i;
         }
-        if (incm) break;
-        base -= 32;
-      }
-      excl = acc;
-      if (lane < k) P.ws.cinc[(uint64_t)t * k + lane] = acc + tot;
-      __syncwarp();
-      if (lane == 0) {
-        __threadfence();
-        st_release32(&P.ws.flag1[t], 2u);
+        excl = (uint32_t)acc;
+        st_release64(dsc, FLAG_P | (acc + tot));
       }
     }
     if (lane < k) {
@@ -559,6 +550,50 @@ __device__ __forceinline__ MP compose(const MP& f, const MP& g) {  // g after f
   return MP{f.A + g.A, fmax(f.C + g.A, g.C)};
 }
 
+// Warp-cooperative decoupled look-back (all 32 lanes of one warp): lane i
+// inspects predecessor tile base-i, so one round trip covers 32
+// predecessors.  `op(earlier, later)` is the scan's associative operator
+// (not necessarily commutative); each window is reduced in tile order with
+// shuffles.  load(p, inclusive) reads tile p's published value after its flag.
+__device__ __forceinline__ double shfl_dn(double v, int o) { return __shfl_down_sync(0xffffffffu, v, o); }
+__device__ __forceinline__ double shfl_ix(double v, int l) { return __shfl_sync(0xffffffffu, v, l); }
+__device__ __forceinline__ MP shfl_dn(const MP& v, int o) {
+  return MP{__shfl_down_sync(0xffffffffu, v.A, o), __shfl_down_sync(0xffffffffu, v.C, o)};
+}
+__device__ __forceinline__ MP shfl_ix(const MP& v, int l) {
+  return MP{__shfl_sync(0xffffffffu, v.A, l), __shfl_sync(0xffffffffu, v.C, l)};
+}
+
+template <class T, class Load, class Op>
+__device__ __forceinline__ T warp_lookback(const uint32_t* flag, int64_t t, T identity, Load load,
+                                           Op op) {
+  const uint32_t lane = threadIdx.x & 31;
+  T acc = identity;  // composition of the windows already visited (the later part)
+  int64_t base = t - 1;
+  while (true) {
+    const int64_t p = base - (int64_t)lane;
+    uint32_t f = 2;
+    T v = identity;
+    if (p >= 0) {
+      do {
+        f = ld_acquire32(&flag[p]);
+      } while (f == 0);
+      v = load(p, f == 2);
+    }
+    const uint32_t incm = __ballot_sync(0xffffffffu, f == 2);
+    const uint32_t last = incm ? (uint32_t)(__ffs(incm) - 1) : 31u;
+    if (lane > last) v = identity;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const T other = shfl_dn(v, o);
+      if (lane + o <= last) v = op(other, v);
+    }
+    acc = op(shfl_ix(v, 0), acc);  // lane 0: v[last] then ... then v[0]
+    if (incm) return acc;
+    base -= 32;
+  }
+}
+
 __global__ void __launch_bounds__(LB) lindley_scan_kernel(LArgs L) {
   __shared__ MP s_w[LB / 32];
   __shared__ MP s_prefix;
@@ -601,45 +636,34 @@ __global__ void __launch_bounds__(LB) lindley_scan_kernel(LArgs L) {
       double b2 = 0.0;
       for (int w2 = 0; w2 < LB / 32; ++w2) b2 += s_busy[w2];
       L.busy_part[blk] = b2;
-      MP pre{0.0, -CUDART_INF};
       if (blk == 0) {
         L.incA[0] = agg.A;
         L.incC[0] = agg.C;
-        __threadfence();
-        st_release32(&L.flag[0], 2);
       } else {
         L.aggA[blk] = agg.A;
         L.aggC[blk] = agg.C;
-        __threadfence();
-        st_release32(&L.flag[blk], 1);
-        MP acc{0.0, -CUDART_INF};  // composition of visited predecessors (later ones first)
-        int64_t p = (int64_t)blk - 1;
-        while (true) {
-          uint32_t fl;
-          do {
-            fl = ld_acquire32(&L.flag[p]);
-          } while (fl == 0);
-          MP v;
-          if (fl == 2) {
-            v.A = *(volatile double*)&L.incA[p];
-            v.C = *(volatile double*)&L.incC[p];
-            acc = compose(v, acc);
-            break;
-          }
-          v.A = *(volatile double*)&L.aggA[p];
-          v.C = *(volatile double*)&L.aggC[p];
-          acc = compose(v, acc);
-          --p;
-        }
-        pre = acc;
+      }
+      __threadfence();
+      st_release32(&L.flag[blk], blk == 0 ? 2u : 1u);
+    }
+    MP pre{0.0, -CUDART_INF};
+    if (blk > 0) {
+      pre = warp_lookback(
+          L.flag, blk, MP{0.0, -CUDART_INF},
+          [&](int64_t p, bool inc) {
+            return inc ? MP{*(volatile double*)&L.incA[p], *(volatile double*)&L.incC[p]}
+                       : MP{*(volatile double*)&L.aggA[p], *(volatile double*)&L.aggC[p]};
+          },
+          [](const MP& a, const MP& b) { return compose(a, b); });
+      if (lane == 0) {
         const MP inc = compose(pre, agg);
         L.incA[blk] = inc.A;
         L.incC[blk] = inc.C;
         __threadfence();
         st_release32(&L.flag[blk], 2);
       }
-      s_prefix = pre;
     }
+    if (lane == 0) s_prefix = pre;
   }
   __syncthreads();
   // exclusive prefix of this thread = block prefix, earlier warps, earlier lanes
@@ -766,6 +790,22 @@ struct SegV {
   uint32_t hp;   // 1 + index of the latest head (0 = none)
   uint32_t hf;   // contains a head
 };
+__device__ __forceinline__ SegV shfl_dn(const SegV& v, int o) {
+  SegV r;
+  r.m.i0 = __shfl_down_sync(0xffffffffu, v.m.i0, o);
+  r.m.i1 = __shfl_down_sync(0xffffffffu, v.m.i1, o);
+  r.hp = __shfl_down_sync(0xffffffffu, v.hp, o);
+  r.hf = __shfl_down_sync(0xffffffffu, v.hf, o);
+  return r;
+}
+__device__ __forceinline__ SegV shfl_ix(const SegV& v, int l) {
+  SegV r;
+  r.m.i0 = __shfl_sync(0xffffffffu, v.m.i0, l);
+  r.m.i1 = __shfl_sync(0xffffffffu, v.m.i1, l);
+  r.hp = __shfl_sync(0xffffffffu, v.hp, l);
+  r.hf = __shfl_sync(0xffffffffu, v.hf, l);
+  return r;
+}
 __device__ __forceinline__ SegV scomb(const SegV& x, const SegV& y) {  // y after x
   SegV r;
   r.m = y.hf ? y.m : pcompose(x.m, y.m);
@@ -814,45 +854,42 @@ __global__ void __launch_bounds__(LB) binade_scan_kernel(BArgs A) {
   }
   if (lane == 31) s_w[w] = x;
   __syncthreads();
-  if (tid == 0) {
+  if (w == 0) {
     SegV agg{{0, 0}, 0, 0};
     for (int q = 0; q < LB / 32; ++q) agg = scomb(agg, s_w[q]);
-    SegV pre{{0, 0}, 0, 0};
-    if (blk == 0) {
-      A.in0[0] = agg.m.i0; A.in1[0] = agg.m.i1; A.inh[0] = agg.hp; A.inf[0] = agg.hf;
-      __threadfence();
-      st_release32(&A.flag[0], 2);
-    } else {
-      A.ag0[blk] = agg.m.i0; A.ag1[blk] = agg.m.i1; A.agh[blk] = agg.hp; A.agf[blk] = agg.hf;
-      __threadfence();
-      st_release32(&A.flag[blk], 1);
-      SegV run{{0, 0}, 0, 0};
-      int64_t p = (int64_t)blk - 1;
-      while (true) {
-        uint32_t fl;
-        do {
-          fl = ld_acquire32(&A.flag[p]);
-        } while (fl == 0);
-        SegV t;
-        if (fl == 2) {
-          t.m.i0 = *(volatile long long*)&A.in0[p]; t.m.i1 = *(volatile long long*)&A.in1[p];
-          t.hp = *(volatile uint32_t*)&A.inh[p]; t.hf = *(volatile uint32_t*)&A.inf[p];
-          run = scomb(t, run);
-          break;
-        }
-        t.m.i0 = *(volatile long long*)&A.ag0[p]; t.m.i1 = *(volatile long long*)&A.ag1[p];
-        t.hp = *(volatile uint32_t*)&A.agh[p]; t.hf = *(volatile uint32_t*)&A.agf[p];
-        run = scomb(t, run);
-        if (run.hf) break;  // a head resets the map; the head position is the max seen
-        --p;
+    if (lane == 0) {
+      if (blk == 0) {
+        A.in0[0] = agg.m.i0; A.in1[0] = agg.m.i1; A.inh[0] = agg.hp; A.inf[0] = agg.hf;
+      } else {
+        A.ag0[blk] = agg.m.i0; A.ag1[blk] = agg.m.i1; A.agh[blk] = agg.hp; A.agf[blk] = agg.hf;
       }
-      pre = run;
-      const SegV inc = scomb(pre, agg);
-      A.in0[blk] = inc.m.i0; A.in1[blk] = inc.m.i1; A.inh[blk] = inc.hp; A.inf[blk] = inc.hf;
       __threadfence();
-      st_release32(&A.flag[blk], 2);
+      st_release32(&A.flag[blk], blk == 0 ? 2u : 1u);
     }
-    s_pre = pre;
+    SegV pre{{0, 0}, 0, 0};
+    if (blk > 0) {
+      pre = warp_lookback(
+          A.flag, blk, SegV{{0, 0}, 0, 0},
+          [&](int64_t p, bool inc) {
+            SegV t;
+            if (inc) {
+              t.m.i0 = *(volatile long long*)&A.in0[p]; t.m.i1 = *(volatile long long*)&A.in1[p];
+              t.hp = *(volatile uint32_t*)&A.inh[p]; t.hf = *(volatile uint32_t*)&A.inf[p];
+            } else {
+              t.m.i0 = *(volatile long long*)&A.ag0[p]; t.m.i1 = *(volatile long long*)&A.ag1[p];
+              t.hp = *(volatile uint32_t*)&A.agh[p]; t.hf = *(volatile uint32_t*)&A.agf[p];
+            }
+            return t;
+          },
+          [](const SegV& a, const SegV& b) { return scomb(a, b); });
+      if (lane == 0) {
+        const SegV inc = scomb(pre, agg);
+        A.in0[blk] = inc.m.i0; A.in1[blk] = inc.m.i1; A.inh[blk] = inc.hp; A.inf[blk] = inc.hf;
+        __threadfence();
+        st_release32(&A.flag[blk], 2);
+      }
+    }
+    if (lane == 0) s_pre = pre;
   }
   __syncthreads();
   SegV pre = s_pre;
@@ -1061,6 +1098,166 @@ __global__ void collect_kernel(const unsigned long long* __restrict__ key, uint3
   }
 }
 
+
+// ------------------------------------------- device-side exact selection
+// One shared level-1 histogram over [kmin, kmax] (read from device memory),
+// bucket search for every target rank, one collect pass over the union of
+// the target buckets, then a single block refines every target in shared
+// memory -- no host round trip until the results are read back.
+constexpr int kSelMax = 4;
+struct SelState {
+  unsigned long long rank[kSelMax];
+  unsigned long long lo[kSelMax], hi[kSelMax];
+  unsigned long long result[kSelMax];
+  unsigned long long base, top;
+  uint32_t shift, nt, need_collect, overflow, ncand;
+  uint32_t bucket[kSelMax];
+};
+
+__global__ void sel_init_kernel(SelState* S, const unsigned long long* kminmax) {
+  const unsigned long long lo = kminmax[0], hi = kminmax[1];
+  S->base = lo;
+  S->top = hi;
+  const unsigned long long span = hi - lo;
+  const int bits = span ? 64 - __clzll(span) : 0;
+  S->shift = bits > HBITS ? (uint32_t)(bits - HBITS) : 0u;
+  S->ncand = 0;
+  S->overflow = 0;
+}
+
+__global__ void sel_hist_kernel(const unsigned long long* __restrict__ key, uint32_t m,
+                                const SelState* S, uint32_t* __restrict__ hist) {
+  __shared__ uint32_t h[HBINS];
+  for (int i = threadIdx.x; i < HBINS; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  const unsigned long long lo = S->base, hi = S->top;
+  const uint32_t shift = S->shift;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+    const unsigned long long v = key[i];
+    if (v >= lo && v <= hi) atomicAdd(&h[(uint32_t)((v - lo) >> shift)], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < HBINS; i += blockDim.x)
+    if (h[i]) atomicAdd(&hist[i], h[i]);
+}
+
+// prefix over the level-1 histogram; per target: bucket, residual rank, range
+__global__ void __launch_bounds__(1024) sel_find_kernel(SelState* S, const uint32_t* hist,
+                                                        uint32_t cap) {
+  __shared__ unsigned long long ps[HBINS];
+  const int t = threadIdx.x;
+  for (int i = t; i < HBINS; i += blockDim.x) ps[i] = hist[i];
+  __syncthreads();
+  for (int o = 1; o < HBINS; o <<= 1) {  // inclusive Hillis-Steele scan (4096 bins)
+    unsigned long long add[HBINS / 1024];
+    for (int q = 0; q < HBINS / 1024; ++q) {
+      const int i = t + q * 1024;
+      add[q] = i >= o ? ps[i - o] : 0ull;
+    }
+    __syncthreads();
+    for (int q = 0; q < HBINS / 1024; ++q) ps[t + q * 1024] += add[q];
+    __syncthreads();
+  }
+  if (t == 0) {
+    unsigned long long need = 0;
+    S->need_collect = 0;
+    for (uint32_t q = 0; q < S->nt; ++q) {
+      const unsigned long long r = S->rank[q];
+      int lo = 0, hi = HBINS - 1;  // first bucket with inclusive count > r
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (ps[mid] > r) hi = mid;
+        else lo = mid + 1;
+      }
+      const unsigned long long before = lo ? ps[lo - 1] : 0ull;
+      S->rank[q] = r - before;
+      S->bucket[q] = lo;
+      const unsigned long long blo = S->base + ((unsigned long long)lo << S->shift);
+      unsigned long long bhi = blo + ((1ull << S->shift) - 1);
+      if (bhi > S->top || bhi < blo) bhi = S->top;
+      S->lo[q] = blo;
+      S->hi[q] = bhi;
+      if (blo == bhi) {
+        S->result[q] = blo;
+      } else {
+        bool dup = false;
+        for (uint32_t z = 0; z < q; ++z) dup |= S->lo[z] == blo && S->hi[z] != S->lo[z];
+        if (!dup) need += ps[lo] - before;
+        S->need_collect = 1;
+      }
+    }
+    S->overflow = need > cap;
+  }
+}
+
+__global__ void sel_collect_kernel(const unsigned long long* __restrict__ key, uint32_t m,
+                                   SelState* S, unsigned long long* __restrict__ out, uint32_t cap) {
+  if (!S->need_collect || S->overflow) return;
+  unsigned long long lo[kSelMax], hi[kSelMax];
+  const uint32_t nt = S->nt;
+  for (uint32_t q = 0; q < kSelMax; ++q) {
+    lo[q] = q < nt ? S->lo[q] : 1;
+    hi[q] = q < nt && S->lo[q] != S->hi[q] ? S->hi[q] : 0;
+  }
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+    const unsigned long long v = key[i];
+    bool in = false;
+#pragma unroll
+    for (int q = 0; q < kSelMax; ++q) in |= v >= lo[q] && v <= hi[q];
+    if (in) {
+      const uint32_t slot = atomicAdd(&S->ncand, 1u);
+      if (slot < cap) out[slot] = v;
+    }
+  }
+}
+
+// refine every unresolved target on the candidates, all levels in smem
+__global__ void __launch_bounds__(1024) sel_refine_kernel(SelState* S,
+                                                          const unsigned long long* __restrict__ cand) {
+  __shared__ uint32_t h[HBINS];
+  __shared__ unsigned long long s_lo, s_hi, s_rank;
+  if (!S->need_collect || S->overflow) return;
+  const uint32_t m = S->ncand;
+  for (uint32_t q = 0; q < S->nt; ++q) {
+    if (threadIdx.x == 0) {
+      s_lo = S->lo[q];
+      s_hi = S->hi[q];
+      s_rank = S->rank[q];
+    }
+    __syncthreads();
+    while (s_lo < s_hi) {
+      const unsigned long long lo = s_lo, hi = s_hi;
+      const unsigned long long span = hi - lo;
+      const int bits = 64 - __clzll(span);
+      const uint32_t shift = bits > HBITS ? (uint32_t)(bits - HBITS) : 0u;
+      for (int i = threadIdx.x; i < HBINS; i += blockDim.x) h[i] = 0;
+      __syncthreads();
+      for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
+        const unsigned long long v = cand[i];
+        if (v >= lo && v <= hi) atomicAdd(&h[(uint32_t)((v - lo) >> shift)], 1u);
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        unsigned long long acc = 0, r = s_rank;
+        uint32_t b = 0;
+        for (; b < HBINS; ++b) {
+          if (acc + h[b] > r) break;
+          acc += h[b];
+        }
+        s_rank = r - acc;
+        const unsigned long long nlo = lo + ((unsigned long long)b << shift);
+        unsigned long long nhi = nlo + ((1ull << shift) - 1);
+        if (nhi > hi || nhi < nlo) nhi = hi;
+        s_lo = nlo;
+        s_hi = nhi;
+      }
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) S->result[q] = s_lo;
+    __syncthreads();
+  }
+}
+
 // ------------------------------------------------------------------ host
 #define BB_CK(x)                                                                        \
   do {                                                                                  \
@@ -1177,9 +1374,7 @@ void trace_run(const TraceArgs& A, TraceResult* R, cudaStream_t s) {
   BB_CK(cudaEventCreate(&ev1));
   BB_CK(cudaEventCreate(&ev2));
   BB_CK(pool.alloc((void**)&ws.counters, 16));
-  BB_CK(pool.alloc((void**)&ws.flag1, (size_t)ntiles * 4));
-  BB_CK(pool.alloc((void**)&ws.cagg, (size_t)ntiles * k * 4));
-  BB_CK(pool.alloc((void**)&ws.cinc, (size_t)ntiles * k * 4));
+  BB_CK(pool.alloc((void**)&ws.desc1, (size_t)ntiles * k * 8));
   BB_CK(pool.alloc((void**)&ws.desc2v, (size_t)ntiles * k * 8));
   BB_CK(pool.alloc((void**)&ws.desc2f, (size_t)ntiles * k * 4));
   BB_CK(pool.alloc((void**)&ws.pb8, n));
@@ -1195,7 +1390,7 @@ void trace_run(const TraceArgs& A, TraceResult* R, cudaStream_t s) {
   BB_CK(pool.alloc((void**)&ws.err, sizeof(DevError)));
   BB_CK(pool.alloc((void**)&ws.info, sizeof(Info)));
   BB_CK(cudaMemsetAsync(ws.counters, 0, 16, s));
-  BB_CK(cudaMemsetAsync(ws.flag1, 0, (size_t)ntiles * 4, s));
+  BB_CK(cudaMemsetAsync(ws.desc1, 0, (size_t)ntiles * k * 8, s));
   BB_CK(cudaMemsetAsync(ws.desc2f, 0, (size_t)ntiles * k * 4, s));
   BB_CK(cudaMemsetAsync(ws.fin_cnt, 0, 32 * 8, s));
   BB_CK(cudaMemsetAsync(ws.fin_open, 0, 32 * 8, s));
@@ -1425,7 +1620,38 @@ void trace_run(const TraceArgs& A, TraceResult* R, cudaStream_t s) {
         if (idxs[q] + 1 < nc) ranks.push_back(idxs[q] + 1);
       }
       std::vector<unsigned long long> vals;
-      BB_CK(select_ranks(keys, n, mm[0], mm[1], ranks, vals, pool, s));
+      {
+        // device-side selection (single sync); multi-launch refine as the fallback
+        SelState hs{};
+        hs.nt = (uint32_t)ranks.size();
+        for (size_t q = 0; q < ranks.size(); ++q) hs.rank[q] = ranks[q];
+        SelState* ds;
+        uint32_t* dh;
+        unsigned long long* dc;
+        const uint32_t cap = n < (1u << 22) ? n : (1u << 22);
+        BB_CK(pool.alloc((void**)&ds, sizeof(SelState)));
+        BB_CK(pool.alloc((void**)&dh, HBINS * 4));
+        BB_CK(pool.alloc((void**)&dc, (size_t)cap * 8));
+        BB_CK(cudaMemcpyAsync(ds, &hs, sizeof hs, cudaMemcpyHostToDevice, s));
+        BB_CK(cudaMemsetAsync(dh, 0, HBINS * 4, s));
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        sel_init_kernel<<<1, 1, 0, s>>>(ds, kminmax);
+        sel_hist_kernel<<<sms * 4, 256, 0, s>>>(keys, n, ds, dh);
+        sel_find_kernel<<<1, 1024, 0, s>>>(ds, dh, cap);
+        sel_collect_kernel<<<sms * 4, 256, 0, s>>>(keys, n, ds, dc, cap);
+        sel_refine_kernel<<<1, 1024, 0, s>>>(ds, dc);
+        note_launch(5);
+        BB_CK(cudaGetLastError());
+        BB_CK(cudaMemcpyAsync(&hs, ds, sizeof hs, cudaMemcpyDeviceToHost, s));
+        BB_CK(cudaStreamSynchronize(s));
+        if (hs.overflow) {
+          BB_CK(select_ranks(keys, n, mm[0], mm[1], ranks, vals, pool, s));
+        } else {
+          for (size_t q = 0; q < ranks.size(); ++q) vals.push_back(hs.result[q]);
+        }
+      }
       size_t vi = 0;
       double outq[2];
       for (int q = 0; q < 2; ++q) {
