@@ -18,6 +18,7 @@
 //   * n_servers > 1, max_batch_wait and > 32 bins (single runs) throw
 //     std::logic_error("...not implemented on the GPU path yet").
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <limits>

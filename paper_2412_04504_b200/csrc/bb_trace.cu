@@ -124,6 +124,9 @@ __global__ void __launch_bounds__(TB) partition_kernel(PartArgs P) {
   __shared__ unsigned long long s_slot[TILE + 32];
   __shared__ uint32_t s_wclose[NW];
   __shared__ uint32_t s_closebase, s_tile, s_flags, s_nfrag_total;
+  __shared__ unsigned long long s_lbsum[NW][32], s_acc[32];
+  __shared__ uint8_t s_lbfound[NW][32], s_bdone[32];
+  __shared__ int s_lbdone;
 
   const uint32_t tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const uint32_t k = P.k, n = P.n, B = P.B;
@@ -218,48 +221,75 @@ __global__ void __launch_bounds__(TB) partition_kernel(PartArgs P) {
   __syncthreads();
   if (tid == 0 && s_flags) atomicOr(P.ws.flags, s_flags);
 
-  if (w == 0) {
-    uint32_t excl = 0, tot = 0, nfrag = 0;
-    if (lane < k) {
-      uint32_t run = 0;
-      for (int w2 = 0; w2 < NW; ++w2) {
-        s_woff[w2][lane] = run;
-        run += s_wcnt[w2][lane];
-      }
-      tot = run;
-      s_tot[lane] = tot;
+  if (w == 0 && lane < k) {
+    uint32_t run = 0;
+    for (int w2 = 0; w2 < NW; ++w2) {
+      s_woff[w2][lane] = run;
+      run += s_wcnt[w2][lane];
     }
-    // phase-1 decoupled look-back, one bin per lane: each round trip loads
-    // the packed (flag | count) words of kLookWin predecessors for the lane's bin
-    if (lane < k) {
-      unsigned long long* dsc = P.ws.desc1 + (uint64_t)t * k + lane;
-      if (t == 0) {
-        st_release64(dsc, FLAG_P | tot);
-      } else {
-        st_release64(dsc, FLAG_A | tot);
-        unsigned long long acc = 0;
-        int64_t p = (int64_t)t - 1;
-        bool done = false;
-        while (!done) {
-          unsigned long long v[kLookWin];
+    s_tot[lane] = run;
+    st_release64(P.ws.desc1 + (uint64_t)t * k + lane, (t == 0 ? FLAG_P : FLAG_A) | run);
+  }
+  if (tid < 32) {
+    s_acc[tid] = 0;
+    s_bdone[tid] = tid >= k;
+  }
+  __syncthreads();
+  // phase-1 decoupled look-back with the whole block: warp w inspects
+  // predecessors base-w*kLookWin .. base-w*kLookWin-(kLookWin-1), one bin
+  // per lane, so a round trip covers NW*kLookWin predecessors; the windows
+  // are combined nearest-first in shared memory and stop at the first
+  // inclusive prefix of each bin.
+  if (t > 0) {
+    int64_t base = (int64_t)t - 1;
+    while (true) {
+      unsigned long long sum = 0;
+      uint8_t found = 0;
+      if (lane < k && !s_bdone[lane]) {
+        const int64_t p0 = base - (int64_t)w * kLookWin;
+        unsigned long long v[kLookWin];
 #pragma unroll
-          for (int i = 0; i < kLookWin; ++i)
-            v[i] = p - i >= 0 ? ld_relaxed64(P.ws.desc1 + (uint64_t)(p - i) * k + lane) : FLAG_P;
-          int i = 0;
-          for (; i < kLookWin; ++i) {
-            const unsigned long long f = v[i] >> 62;
-            if (f == 0) break;          // not yet published: reload from here
-            acc += v[i] & VAL_MASK;
-            if (f == 2) {
-              done = true;
+        for (int i = 0; i < kLookWin; ++i)
+          v[i] = p0 - i >= 0 ? ld_relaxed64(P.ws.desc1 + (uint64_t)(p0 - i) * k + lane) : FLAG_P;
+        for (int i = 0; i < kLookWin; ++i) {
+          unsigned long long x = v[i];
+          while ((x >> 62) == 0) x = ld_relaxed64(P.ws.desc1 + (uint64_t)(p0 - i) * k + lane);
+          sum += x & VAL_MASK;
+          if ((x >> 62) == 2) {
+            found = 1;
+            break;
+          }
+        }
+      }
+      s_lbsum[w][lane] = sum;
+      s_lbfound[w][lane] = found;
+      __syncthreads();
+      if (w == 0) {
+        if (lane < k && !s_bdone[lane]) {
+          unsigned long long acc = s_acc[lane];
+          for (int w2 = 0; w2 < NW; ++w2) {
+            acc += s_lbsum[w2][lane];
+            if (s_lbfound[w2][lane]) {
+              s_bdone[lane] = 1;
               break;
             }
           }
-          p -= i;
+          s_acc[lane] = acc;
         }
-        excl = (uint32_t)acc;
-        st_release64(dsc, FLAG_P | (acc + tot));
+        const bool all = __all_sync(0xffffffffu, lane >= k || s_bdone[lane]);
+        if (lane == 0) s_lbdone = all;
       }
+      __syncthreads();
+      if (s_lbdone) break;
+      base -= (int64_t)NW * kLookWin;
+    }
+  }
+  if (w == 0) {
+    uint32_t excl = 0, tot = 0, nfrag = 0;
+    if (lane < k) {
+      tot = s_tot[lane];
+      excl = (uint32_t)s_acc[lane];
+      if (t > 0) st_release64(P.ws.desc1 + (uint64_t)t * k + lane, FLAG_P | (excl + tot));
     }
     if (lane < k) {
       const uint32_t jlo = P.divB.div(excl);
@@ -1190,6 +1220,72 @@ __global__ void __launch_bounds__(1024) sel_find_kernel(SelState* S, const uint3
   }
 }
 
+// level 2 over the full key array: every unresolved target's bucket split
+// into 2048 sub-buckets at once (per-target shared histograms)
+constexpr int kSub = 2048;
+__global__ void sel_hist2_kernel(const unsigned long long* __restrict__ key, uint32_t m,
+                                 const SelState* S, uint32_t* __restrict__ hist2) {
+  __shared__ uint32_t h[kSelMax][kSub];
+  __shared__ unsigned long long s_lo[kSelMax], s_hi[kSelMax];
+  __shared__ uint32_t s_sh[kSelMax];
+  for (int i = threadIdx.x; i < kSelMax * kSub; i += blockDim.x) (&h[0][0])[i] = 0;
+  if (threadIdx.x < kSelMax) {
+    const uint32_t q = threadIdx.x;
+    const bool live = q < S->nt && S->lo[q] != S->hi[q];
+    s_lo[q] = live ? S->lo[q] : 1;
+    s_hi[q] = live ? S->hi[q] : 0;
+    const unsigned long long span = live ? S->hi[q] - S->lo[q] : 0;
+    const int bits = span ? 64 - __clzll(span) : 0;
+    s_sh[q] = bits > 11 ? (uint32_t)(bits - 11) : 0u;
+  }
+  __syncthreads();
+  if (!S->need_collect) return;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+    const unsigned long long v = key[i];
+#pragma unroll
+    for (int q = 0; q < kSelMax; ++q)
+      if (v >= s_lo[q] && v <= s_hi[q]) atomicAdd(&h[q][(uint32_t)((v - s_lo[q]) >> s_sh[q])], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kSelMax * kSub; i += blockDim.x)
+    if ((&h[0][0])[i]) atomicAdd(&hist2[i], (&h[0][0])[i]);
+}
+
+// narrow every unresolved target to its level-2 sub-bucket
+__global__ void sel_find2_kernel(SelState* S, const uint32_t* hist2, uint32_t cap) {
+  if (threadIdx.x != 0 || !S->need_collect) return;
+  unsigned long long need = 0;
+  uint32_t live = 0;
+  for (uint32_t q = 0; q < S->nt; ++q) {
+    if (S->lo[q] == S->hi[q]) continue;
+    const unsigned long long span = S->hi[q] - S->lo[q];
+    const int bits = 64 - __clzll(span);
+    const uint32_t sh = bits > 11 ? (uint32_t)(bits - 11) : 0u;
+    unsigned long long acc = 0, r = S->rank[q];
+    uint32_t b = 0;
+    for (; b < kSub; ++b) {
+      if (acc + hist2[q * kSub + b] > r) break;
+      acc += hist2[q * kSub + b];
+    }
+    S->rank[q] = r - acc;
+    const unsigned long long nlo = S->lo[q] + ((unsigned long long)b << sh);
+    unsigned long long nhi = nlo + ((1ull << sh) - 1);
+    if (nhi > S->hi[q] || nhi < nlo) nhi = S->hi[q];
+    S->lo[q] = nlo;
+    S->hi[q] = nhi;
+    if (nlo == nhi) {
+      S->result[q] = nlo;
+    } else {
+      bool dup = false;
+      for (uint32_t z = 0; z < q; ++z) dup |= S->lo[z] == nlo && S->hi[z] == nhi;
+      if (!dup) need += hist2[q * kSub + b];
+      ++live;
+    }
+  }
+  S->need_collect = live != 0;
+  S->overflow = need > cap;
+}
+
 __global__ void sel_collect_kernel(const unsigned long long* __restrict__ key, uint32_t m,
                                    SelState* S, unsigned long long* __restrict__ out, uint32_t cap) {
   if (!S->need_collect || S->overflow) return;
@@ -1639,10 +1735,15 @@ void trace_run(const TraceArgs& A, TraceResult* R, cudaStream_t s) {
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         sel_init_kernel<<<1, 1, 0, s>>>(ds, kminmax);
         sel_hist_kernel<<<sms * 4, 256, 0, s>>>(keys, n, ds, dh);
-        sel_find_kernel<<<1, 1024, 0, s>>>(ds, dh, cap);
+        sel_find_kernel<<<1, 1024, 0, s>>>(ds, dh, 0xFFFFFFFFu);
+        uint32_t* dh2;
+        BB_CK(pool.alloc((void**)&dh2, (size_t)kSelMax * kSub * 4));
+        BB_CK(cudaMemsetAsync(dh2, 0, (size_t)kSelMax * kSub * 4, s));
+        sel_hist2_kernel<<<sms * 2, 512, 0, s>>>(keys, n, ds, dh2);
+        sel_find2_kernel<<<1, 32, 0, s>>>(ds, dh2, cap);
         sel_collect_kernel<<<sms * 4, 256, 0, s>>>(keys, n, ds, dc, cap);
         sel_refine_kernel<<<1, 1024, 0, s>>>(ds, dc);
-        note_launch(5);
+        note_launch(7);
         BB_CK(cudaGetLastError());
         BB_CK(cudaMemcpyAsync(&hs, ds, sizeof hs, cudaMemcpyDeviceToHost, s));
         BB_CK(cudaStreamSynchronize(s));
