@@ -1220,6 +1220,50 @@ __global__ void __launch_bounds__(1024) sel_find_kernel(SelState* S, const uint3
   }
 }
 
+
+// Block-wide bucket search (blockDim == 1024): the bucket b of h[0..nb) with
+// prefix(b) <= r < prefix(b) + h[b]; writes *bucket and *before.
+__device__ __forceinline__ void block_find(const uint32_t* h, int nb, unsigned long long r,
+                                           uint32_t* bucket, unsigned long long* before) {
+  __shared__ unsigned long long s_ws[32];
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const int per = nb / 1024;
+  unsigned long long loc = 0;
+  for (int i = 0; i < per; ++i) loc += h[t * per + i];
+  unsigned long long x = loc;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_ws[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    unsigned long long v = s_ws[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long y = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += y;
+    }
+    s_ws[lane] = v;  // inclusive per warp
+  }
+  __syncthreads();
+  const unsigned long long excl = x - loc + (w ? s_ws[w - 1] : 0ull);
+  if (r >= excl && r < excl + loc) {
+    unsigned long long acc = excl;
+    for (int i = 0; i < per; ++i) {
+      const uint32_t c = h[t * per + i];
+      if (r < acc + c) {
+        *bucket = (uint32_t)(t * per + i);
+        *before = acc;
+        break;
+      }
+      acc += c;
+    }
+  }
+  __syncthreads();
+}
+
 // level 2 over the full key array: every unresolved target's bucket split
 // into 2048 sub-buckets at once (per-target shared histograms)
 constexpr int kSub = 2048;
@@ -1251,39 +1295,43 @@ __global__ void sel_hist2_kernel(const unsigned long long* __restrict__ key, uin
     if ((&h[0][0])[i]) atomicAdd(&hist2[i], (&h[0][0])[i]);
 }
 
-// narrow every unresolved target to its level-2 sub-bucket
-__global__ void sel_find2_kernel(SelState* S, const uint32_t* hist2, uint32_t cap) {
-  if (threadIdx.x != 0 || !S->need_collect) return;
-  unsigned long long need = 0;
-  uint32_t live = 0;
+// narrow every unresolved target to its level-2 sub-bucket (1024 threads)
+__global__ void __launch_bounds__(1024) sel_find2_kernel(SelState* S, const uint32_t* hist2,
+                                                         uint32_t cap) {
+  __shared__ uint32_t s_b;
+  __shared__ unsigned long long s_before;
+  if (!S->need_collect) return;
   for (uint32_t q = 0; q < S->nt; ++q) {
-    if (S->lo[q] == S->hi[q]) continue;
-    const unsigned long long span = S->hi[q] - S->lo[q];
-    const int bits = 64 - __clzll(span);
-    const uint32_t sh = bits > 11 ? (uint32_t)(bits - 11) : 0u;
-    unsigned long long acc = 0, r = S->rank[q];
-    uint32_t b = 0;
-    for (; b < kSub; ++b) {
-      if (acc + hist2[q * kSub + b] > r) break;
-      acc += hist2[q * kSub + b];
+    if (S->lo[q] == S->hi[q]) continue;  // uniform across the block
+    block_find(hist2 + q * kSub, kSub, S->rank[q], &s_b, &s_before);
+    if (threadIdx.x == 0) {
+      const unsigned long long span = S->hi[q] - S->lo[q];
+      const int bits = 64 - __clzll(span);
+      const uint32_t sh = bits > 11 ? (uint32_t)(bits - 11) : 0u;
+      S->rank[q] -= s_before;
+      const unsigned long long nlo = S->lo[q] + ((unsigned long long)s_b << sh);
+      unsigned long long nhi = nlo + ((1ull << sh) - 1);
+      if (nhi > S->hi[q] || nhi < nlo) nhi = S->hi[q];
+      S->lo[q] = nlo;
+      S->hi[q] = nhi;
+      if (nlo == nhi) S->result[q] = nlo;
+      S->bucket[q] = hist2[q * kSub + s_b];  // candidate count of the sub-bucket
     }
-    S->rank[q] = r - acc;
-    const unsigned long long nlo = S->lo[q] + ((unsigned long long)b << sh);
-    unsigned long long nhi = nlo + ((1ull << sh) - 1);
-    if (nhi > S->hi[q] || nhi < nlo) nhi = S->hi[q];
-    S->lo[q] = nlo;
-    S->hi[q] = nhi;
-    if (nlo == nhi) {
-      S->result[q] = nlo;
-    } else {
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    unsigned long long need = 0;
+    uint32_t live = 0;
+    for (uint32_t q = 0; q < S->nt; ++q) {
+      if (S->lo[q] == S->hi[q]) continue;
       bool dup = false;
-      for (uint32_t z = 0; z < q; ++z) dup |= S->lo[z] == nlo && S->hi[z] == nhi;
-      if (!dup) need += hist2[q * kSub + b];
+      for (uint32_t z = 0; z < q; ++z) dup |= S->lo[z] == S->lo[q] && S->hi[z] == S->hi[q];
+      if (!dup) need += S->bucket[q];
       ++live;
     }
+    S->need_collect = live != 0;
+    S->overflow = need > cap;
   }
-  S->need_collect = live != 0;
-  S->overflow = need > cap;
 }
 
 __global__ void sel_collect_kernel(const unsigned long long* __restrict__ key, uint32_t m,
@@ -1333,15 +1381,12 @@ __global__ void __launch_bounds__(1024) sel_refine_kernel(SelState* S,
         if (v >= lo && v <= hi) atomicAdd(&h[(uint32_t)((v - lo) >> shift)], 1u);
       }
       __syncthreads();
+      __shared__ uint32_t s_b;
+      __shared__ unsigned long long s_before;
+      block_find(h, HBINS, s_rank, &s_b, &s_before);
       if (threadIdx.x == 0) {
-        unsigned long long acc = 0, r = s_rank;
-        uint32_t b = 0;
-        for (; b < HBINS; ++b) {
-          if (acc + h[b] > r) break;
-          acc += h[b];
-        }
-        s_rank = r - acc;
-        const unsigned long long nlo = lo + ((unsigned long long)b << shift);
+        s_rank -= s_before;
+        const unsigned long long nlo = lo + ((unsigned long long)s_b << shift);
         unsigned long long nhi = nlo + ((1ull << shift) - 1);
         if (nhi > hi || nhi < nlo) nhi = hi;
         s_lo = nlo;
@@ -1740,7 +1785,7 @@ void trace_run(const TraceArgs& A, TraceResult* R, cudaStream_t s) {
         BB_CK(pool.alloc((void**)&dh2, (size_t)kSelMax * kSub * 4));
         BB_CK(cudaMemsetAsync(dh2, 0, (size_t)kSelMax * kSub * 4, s));
         sel_hist2_kernel<<<sms * 2, 512, 0, s>>>(keys, n, ds, dh2);
-        sel_find2_kernel<<<1, 32, 0, s>>>(ds, dh2, cap);
+        sel_find2_kernel<<<1, 1024, 0, s>>>(ds, dh2, cap);
         sel_collect_kernel<<<sms * 4, 256, 0, s>>>(keys, n, ds, dc, cap);
         sel_refine_kernel<<<1, 1024, 0, s>>>(ds, dc);
         note_launch(7);
