@@ -218,6 +218,7 @@ def main():
     ap.add_argument("--ref-reps", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-trace", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", help="nccl (default) or gloo for testing")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference_arm(args)
@@ -230,10 +231,14 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:  # functional testing of the N>1 path on a single GPU
+            dist.init_process_group(args.dist_backend)
     stream = torch.cuda.current_stream()
     sptr = stream.cuda_stream
 
@@ -331,9 +336,12 @@ def main():
     if kernel_ms:
         achieved = instr / (kernel_ms / 1e3)
         traffic = None
-        prof = os.path.join(ROOT, "profiles", "gen_kernel_ncu.json")
-        if os.path.exists(prof):
-            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+        prof = os.path.join(ROOT, "profiles", "r01_gen_kernel_ncu.json")
+        if os.path.exists(prof):  # one `ncu --set full` capture at 1500 replications/point
+            cap = json.load(open(prof))
+            cap = cap[0] if isinstance(cap, list) else cap
+            if cap.get("dram_bytes_per_launch") is not None:
+                traffic = cap["dram_bytes_per_launch"] * R / 1500.0
         roofline = {
             "bound": "issue", "kernel": "gen_kernel",
             "achieved": achieved / 1e9, "peak": peak / 1e9, "unit": "Glane-instr/s",

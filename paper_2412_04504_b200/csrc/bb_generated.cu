@@ -145,21 +145,51 @@ struct Rep {
   uint64_t ncomp;
 };
 
+// S servers' free times (multi-server runs only), strided per thread.
+struct Servers {
+  uint32_t S;
+  double* V;
+  uint32_t stride;
+};
+
+// dispatch, simulator.hpp:256-267: a batch formed at R.t starts when a server
+// is free (FIFO: the Kiefer-Wolfowitz recursion; with one server the Lindley
+// step D = max(D, R) + S, and D is also the last completion).
+__device__ __forceinline__ void dispatch(Rep& R, const Servers& sv, double S, uint32_t members) {
+  double fin;
+  if (sv.S == 1) {
+    fin = R.D = __dadd_rn(fmax(R.D, R.t), S);
+  } else {
+    double vmin = sv.V[0];
+    uint32_t im = 0;
+    for (uint32_t q = 1; q < sv.S; ++q) {
+      const double v = sv.V[(size_t)q * sv.stride];
+      if (v < vmin) {
+        vmin = v;
+        im = q;
+      }
+    }
+    fin = __dadd_rn(fmax(vmin, R.t), S);
+    sv.V[(size_t)im * sv.stride] = fin;
+    R.D = fmax(R.D, fin);  // last completion (simulator.hpp:275)
+  }
+  R.busy += S;
+  R.latw += (double)members * fin;
+  R.ncomp += members;
+}
+
 // One request folded into its bin; closes the batch at B members
-// (on_arrival + form_batch + dispatch, simulator.hpp:187-267, one server).
+// (on_arrival + form_batch, simulator.hpp:187-254).
 template <int SVC, bool track>
 __device__ __forceinline__ void fold(Rep& R, uint64_t* __restrict__ slot, double* __restrict__ osum,
- uint64_t xs, uint32_t B, const SvcParams& svc) {
+                                     uint64_t xs, uint32_t B, const SvcParams& svc,
+                                     const Servers& sv) {
   const uint64_t s0 = *slot;
   const uint64_t km = max(s0 & ~kCntMask, xs << kCntBits);
   const uint32_t cnt = (uint32_t)(s0 & kCntMask) + 1;
   if (cnt == B) {
     *slot = 0;
-    const double S = svc_of_key_t<SVC>(svc, km >> kCntBits);
-    R.D = __dadd_rn(fmax(R.D, R.t), S);
-    R.busy += S;
-    R.latw += (double)B * R.D;
-    R.ncomp += B;
+    dispatch(R, sv, svc_of_key_t<SVC>(svc, km >> kCntBits), B);
     if (track) *osum = 0.0;
   } else {
     *slot = km | cnt;
@@ -169,6 +199,9 @@ __device__ __forceinline__ void fold(Rep& R, uint64_t* __restrict__ slot, double
 
 #ifndef BB_GEN_MINB
 #define BB_GEN_MINB 1
+#endif
+#ifndef BB_GEN_PIPE
+#define BB_GEN_PIPE 0  // software-pipeline the next group's draws (A/B: slower, 134 regs)
 #endif
 #ifndef BB_GEN_UNROLL
 #define BB_GEN_UNROLL 4  // requests in flight per thread (even)
@@ -257,23 +290,55 @@ __global__ void __launch_bounds__(kGenThreads, BB_GEN_MINB) gen_kernel(const __g
         if (track)
           for (uint32_t b = 0; b < k; ++b) s_osum[b * kGenThreads + tid] = 0.0;
         Rep R{0.0, 0.0, 0.0, 0.0, 0.0, 0};
+        Servers srv{P.n_servers ? P.n_servers : 1u, nullptr, 0};
+        if (srv.S > 1) {  // all servers idle at t = 0
+          srv.stride = gridDim.x * blockDim.x;
+          srv.V = L.srv + (size_t)blockIdx.x * blockDim.x + tid;
+          for (uint32_t q = 0; q < srv.S; ++q) srv.V[(size_t)q * srv.stride] = 0.0;
+        }
         uint32_t cyc0 = 0;
         const double a0 = exp1_from_bits53_c(draw<SVC>(cyc_rank, nt, 0, c2, c3, cyc0).xg, L.coef) * inv_lambda;
         // U requests per iteration: their draws, exponentials and bins are
         // independent, so the latencies overlap; the folds stay in order
         constexpr int U = BB_GEN_UNROLL;
+        // software pipeline: the next group's Philox blocks (integer pipes)
+        // are issued in the same basic block as this group's exponentials
+        // (fp64 pipe) so the scheduler interleaves them (cyclic traces keep a
+        // running table index and are not pipelined)
+        constexpr bool PIPE = BB_GEN_PIPE && SVC != kSvcCyclic;
         uint32_t i = 0;
-        for (; i + U <= n; i += U) {
-          Draw d[U];
-          uint64_t e[U];
-          double g[U];
-          uint32_t pb[U];
+        Draw d[U];
+        uint64_t e[U];
+        if (PIPE && U <= n) {
 #pragma unroll
-          for (int u = 0; u < U; ++u) d[u] = draw<SVC>(cyc_rank, nt, i + u, c2, c3, cyc);
+          for (int u = 0; u < U; ++u) d[u] = draw<SVC>(cyc_rank, nt, u, c2, c3, cyc);
 #pragma unroll
           for (int u = 0; u < U; u += 2) {
             e[u] = e[u + 1] = 0;
-            err_pair(i + u, e[u], e[u + 1]);
+            err_pair(u, e[u], e[u + 1]);
+          }
+        }
+        for (; i + U <= n; i += U) {
+          double g[U];
+          uint32_t pb[U];
+          Draw dn[U];
+          uint64_t en[U];
+          if (!PIPE) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) d[u] = draw<SVC>(cyc_rank, nt, i + u, c2, c3, cyc);
+#pragma unroll
+            for (int u = 0; u < U; u += 2) {
+              e[u] = e[u + 1] = 0;
+              err_pair(i + u, e[u], e[u + 1]);
+            }
+          } else {
+#pragma unroll
+            for (int u = 0; u < U; ++u) dn[u] = draw<SVC>(cyc_rank, nt, i + U + u, c2, c3, cyc);
+#pragma unroll
+            for (int u = 0; u < U; u += 2) {
+              en[u] = en[u + 1] = 0;
+              err_pair(i + U + u, en[u], en[u + 1]);
+            }
           }
 #pragma unroll
           for (int u = 0; u < U; ++u) g[u] = exp1_from_bits53_c(d[u].xg, L.coef) * inv_lambda;
@@ -297,7 +362,14 @@ __global__ void __launch_bounds__(kGenThreads, BB_GEN_MINB) gen_kernel(const __g
             R.t += g[u];  // exponential inter-arrival, simulator.hpp:181
             R.asum += R.t;
             fold<SVC, TRACK>(R, st + (pb[u] - 1) * kGenThreads + tid,
-                             s_osum + (pb[u] - 1) * kGenThreads + tid, d[u].xs, B, svc);
+                             s_osum + (pb[u] - 1) * kGenThreads + tid, d[u].xs, B, svc, srv);
+          }
+          if (PIPE) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              d[u] = dn[u];
+              e[u] = en[u];
+            }
           }
         }
         // tail: fewer than U requests left, one at a time
@@ -314,7 +386,7 @@ __global__ void __launch_bounds__(kGenThreads, BB_GEN_MINB) gen_kernel(const __g
             R.t += exp1_from_bits53_c(d0.xg, L.coef) * inv_lambda;
             R.asum += R.t;
             fold<SVC, TRACK>(R, st + (p0 - 1) * kGenThreads + tid, s_osum + (p0 - 1) * kGenThreads + tid,
-                      d0.xs, B, svc);
+                      d0.xs, B, svc, srv);
           }
         }
         double leftover = 0.0;
@@ -324,11 +396,7 @@ __global__ void __launch_bounds__(kGenThreads, BB_GEN_MINB) gen_kernel(const __g
             const uint32_t cnt = (uint32_t)(s0 & kCntMask);
             if (!cnt) continue;
             if (flush) {  // on_drain partials at the last arrival, bin order
-              const double S = svc_of_key_t<SVC>(svc, s0 >> kCntBits);
-              R.D = __dadd_rn(fmax(R.D, R.t), S);
-              R.busy += S;
-              R.latw += (double)cnt * R.D;
-              R.ncomp += cnt;
+              dispatch(R, srv, svc_of_key_t<SVC>(svc, s0 >> kCntBits), cnt);
             } else {
               leftover += s_osum[b * kGenThreads + tid];
             }
@@ -337,7 +405,7 @@ __global__ void __launch_bounds__(kGenThreads, BB_GEN_MINB) gen_kernel(const __g
         if (!failed && R.ncomp > 0) {  // finish(), simulator.hpp:279-301
           mk_out = R.D - a0;
           thr_out = (double)R.ncomp / mk_out;
-          busy_out = R.busy / mk_out;
+          busy_out = R.busy / ((double)srv.S * mk_out);  // simulator.hpp:287-288
           lat_out = (R.latw - (R.asum - leftover)) / (double)R.ncomp;
         } else {
           mk_out = thr_out = busy_out = lat_out = failed ? BB_QNAN : 0.0;
@@ -500,9 +568,18 @@ cudaError_t launch_gen(const GenLaunch& L, cudaStream_t s) {
   const uint64_t cap = (uint64_t)sms * occ;
   const unsigned grid = (unsigned)(want < cap ? want : cap);
   if (grid == 0) return cudaSuccess;
-  kern<<<grid, kGenThreads, smem, s>>>(L);
+  GenLaunch L2 = L;
+  double* srv = nullptr;
+  if (L.s_max > 1) {  // free times of S servers per resident thread
+    e = cudaMallocAsync((void**)&srv, (size_t)grid * kGenThreads * L.s_max * sizeof(double), s);
+    if (e != cudaSuccess) return e;
+    L2.srv = srv;
+  }
+  kern<<<grid, kGenThreads, smem, s>>>(L2);
   note_launch();
-  return cudaGetLastError();
+  e = cudaGetLastError();
+  if (srv) cudaFreeAsync(srv, s);
+  return e;
 }
 
 template <int SVC, int ERR>

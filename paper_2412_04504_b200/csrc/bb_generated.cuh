@@ -14,6 +14,7 @@ struct GenPoint {
   uint32_t err_kind;        // 0 perfect, 1 symmetric, 2 confusion
   uint32_t check_domain;    // keys outside [vlo, vhi] raise domain_error
   uint32_t gidx;            // global point index (output row)
+  uint32_t n_servers;       // S (simulator.hpp:68)
   uint64_t vlo, vhi;
   uint64_t e_t1, e_t2;      // symmetric: u < p <=> x < t1 ; u >= 1-p <=> x >= t2
   const double* edges;      // k+1 (device), input of the threshold setup
@@ -42,6 +43,8 @@ struct GenLaunch {
   int32_t track;             // finite rate without flush: track open arrival sums
   double* out;              // [BB_REP_FIELDS][n_points*reps_total]
   AtanhCoef coef;           // exponential-variate polynomial (param space)
+  uint32_t s_max;           // largest n_servers in the launch
+  double* srv;              // server free times scratch (set by gen_run)
   DevError* err;
 };
 

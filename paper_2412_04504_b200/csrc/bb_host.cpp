@@ -871,7 +871,9 @@ void build_sweep(std::vector<bb_run_template> tpl, Sweep& W, cudaStream_t st) {
   for (auto& t : W.tpl) {
     W.spec.push_back(materialize(t, 0));
     const SimSpec& s = W.spec.back();
-    if (s.S != 1) raise(BB_EUNSUPPORTED, "n_servers > 1 is not implemented on the GPU path yet");
+    if (s.S != 1 && std::isinf(s.lambda))
+      raise(BB_EUNSUPPORTED, "n_servers > 1 at overload is not implemented on the GPU path yet");
+    if (s.S > 4096) raise(BB_EUNSUPPORTED, "more than 4096 servers is not supported");
     if (t.has_max_batch_wait) raise(BB_EUNSUPPORTED, "max_batch_wait is not implemented on the GPU path yet");
     if (s.k() > BB_MAX_BINS) raise(BB_EUNSUPPORTED, "more than 64 bins is not supported");
     if (s.B > 2047) raise(BB_EUNSUPPORTED, "batch sizes above 2047 are not supported by the fused kernel");
@@ -918,6 +920,7 @@ void build_sweep(std::vector<bb_run_template> tpl, Sweep& W, cudaStream_t st) {
     g.flush = s.flush;
     g.err_kind = s.error_draws() ? (uint32_t)s.err_kind : 0u;
     g.gidx = (uint32_t)i;
+    g.n_servers = (uint32_t)s.S;
     if (g.err_kind == 1) {
       g.e_t1 = (uint64_t)std::ceil(s.p * 0x1.0p53);
       g.e_t2 = (uint64_t)std::ceil((1.0 - s.p) * 0x1.0p53);
@@ -947,13 +950,14 @@ void launch_sweep(const SweepParams* E, Sweep& W, uint64_t rep_begin, uint64_t r
   for (size_t i = 0; i < P; ++i) {
     if (done[i]) continue;
     std::vector<uint32_t> members;
-    uint32_t kmax = 1;
+    uint32_t kmax = 1, smax = 1;
     for (size_t j = i; j < P; ++j)
       if (!done[j] && keys[j].err == keys[i].err && keys[j].cyc == keys[i].cyc &&
           keys[j].ovl == keys[i].ovl && keys[j].track == keys[i].track) {
         members.push_back((uint32_t)j);
         done[j] = true;
         kmax = std::max(kmax, W.gp[j].k);
+        smax = std::max(smax, W.gp[j].n_servers);
       }
     const bb::GenPoint* base = W.d_pts.as<bb::GenPoint>();
     DBuf grp;
@@ -972,6 +976,7 @@ void launch_sweep(const SweepParams* E, Sweep& W, uint64_t rep_begin, uint64_t r
     L.n_points = (uint32_t)members.size();
     L.points_total = (uint32_t)P;
     L.k_max = kmax;
+    L.s_max = smax;
     L.master = E->seed;
     L.single_seed = 0;
     L.reps_total = (uint32_t)E->replications;
@@ -1070,7 +1075,7 @@ void reference_point_reps(const SweepParams* E, const Sweep& W, std::vector<doub
   rep.assign(BB_REP_FIELDS * P * R, 0.0);
   for (size_t i = 0; i < P; ++i) {
     SimSpec s = W.spec[i];
-    s.S = 1;
+    if (s.S != 1) raise(BB_EUNSUPPORTED, "n_servers > 1 in reference-stream mode is not implemented yet");
     if (s.k() > BB_TRACE_MAX_BINS) raise(BB_EUNSUPPORTED, "more than 32 bins in reference-stream mode");
     for (uint64_t r = 0; r < R; ++r) {
       s.seed = bb::replication_seed(E->seed, r);

@@ -193,3 +193,29 @@ def test_results_independent_of_shards():
     pts = bb.sweep_reduce_device(spec, rep.data_ptr())
     for a, b in zip(whole, pts):
         assert a.throughput_mean == b.throughput_mean and a.latency_std == b.latency_std
+
+
+# ---------------------------------------------------------------- multi-server
+@pytest.mark.parametrize("S,lam,k", [(2, 5.0, 3), (4, 3.0, 2), (64, 5.0, 1)])
+def test_multi_server_vs_reference(S, lam, k):
+    # test_simulator.cpp:60-83 (2 servers), acceptance.cpp criterion 3 (64 servers)
+    B, n = (16, 1003) if S < 64 else (128, 12800)
+    t = template(arrival_rate=lam, n_requests=n, batch_size=B, n_servers=S, bins=bb.BinRule(k=k))
+    p = bb.run_point(t, 21, 2000)
+    thr, lat = ref_stats(dict(arrival_rate=lam, n_requests=n, batch_size=B, n_servers=S,
+                              edges=bb.uniform_boundaries(k, 1.0, 20.0).edges, lo=1.0, hi=20.0),
+                         200 if S < 64 else 40)
+    assert within_3se(p.throughput_mean, p.throughput_std, 2000, thr)
+    assert within_3se(p.latency_mean, p.latency_std, 2000, lat)
+
+
+def test_acceptance_criterion3_latency_formula():
+    # acceptance.cpp:126-165: 64 servers, B=128, U[1,20], lambda in {5,10}, k=1..3, within 5%
+    base = template(n_requests=12800, batch_size=128, n_servers=64)
+    spec = bb.ExperimentSpec(base=base, axes=[bb.SweepAxis("lambda", [5.0, 10.0]),
+                                              bb.SweepAxis("k", [1, 2, 3])],
+                             replications=10, seed=1001)
+    for p in bb.run_experiment(spec):
+        pred = bb.expected_latency(128, p.k, 1.0, 20.0, p.arrival_rate)
+        assert abs(p.latency_mean - pred) / pred < 0.05
+        assert p.analytic_latency == pytest.approx(pred)
