@@ -21,8 +21,12 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
+#include <fstream>
 #include <limits>
 #include <optional>
+#include <ostream>
+#include <sstream>
 #include <stdexcept>
 #include <string>
 #include <variant>
@@ -515,6 +519,126 @@ inline PointResult run_point(const RunTemplate& t, std::uint64_t master_seed,
   spec.replications = replications;
   spec.seed = master_seed;
   return run_experiment(spec).front();
+}
+
+// ---------------------------------------------------------------- output formats
+// Byte-identical to the reference's writers (a caller diffing files sees no
+// change); formatting goes through snprintf: "%.17g" is what an ostream at
+// precision 17 prints, "%.10g" the CSV cells.
+namespace detail {
+inline void put_g(std::string& s, const char* fmt, double v) {
+  char buf[40];
+  std::snprintf(buf, sizeof(buf), fmt, v);
+  s += buf;
+}
+inline std::string csv_number(double v) {  // experiment.hpp:374-380: NaN -> empty cell
+  if (std::isnan(v)) return {};
+  if (std::isinf(v)) return v < 0 ? "-inf" : "inf";
+  std::string s;
+  put_g(s, "%.10g", v);
+  return s;
+}
+}  // namespace detail
+
+// One JSON object per request (simulator.hpp:359-382); unserved requests
+// (flush_partial = false) carry null batch fields.
+inline void write_request_log(const SimResult& result, std::ostream& out) {
+  std::string line;
+  for (const Request& r : result.requests) {
+    line.assign("{\"id\":").append(std::to_string(r.id));
+    line += ",\"arrival\":";
+    detail::put_g(line, "%.17g", r.arrival_time);
+    line += ",\"service\":";
+    detail::put_g(line, "%.17g", r.service_time);
+    line.append(",\"true_bin\":").append(std::to_string(r.true_bin));
+    line.append(",\"predicted_bin\":").append(std::to_string(r.predicted_bin));
+    if (r.batch == kNoBatch) {
+      line += ",\"batch\":null,\"start\":null,\"finish\":null}\n";
+    } else {
+      const BatchRecord& b = result.batches.at(r.batch);
+      line.append(",\"batch\":").append(std::to_string(r.batch)).append(",\"start\":");
+      detail::put_g(line, "%.17g", b.start_time);
+      line += ",\"finish\":";
+      detail::put_g(line, "%.17g", b.finish_time);
+      line += "}\n";
+    }
+    out << line;
+  }
+}
+inline void write_request_log(const SimResult& result, const std::string& path) {
+  std::ofstream f(path);
+  if (!f) throw std::runtime_error("cannot open request log for writing: " + path);
+  write_request_log(result, f);
+}
+
+// Sweep results CSV (experiment.hpp:382-414): one row per point, columns in
+// the order below; empty cells for NaN.
+namespace detail {
+struct CsvColumn {
+  const char* name;
+  std::string (*cell)(const ExperimentSpec&, const PointResult&);
+};
+#define BB_NUM_COL(col, field) \
+  {col, [](const ExperimentSpec&, const PointResult& r) { return csv_number(r.field); }}
+#define BB_INT_COL(col, field) \
+  {col, [](const ExperimentSpec&, const PointResult& r) { return std::to_string(r.field); }}
+inline const std::vector<CsvColumn>& csv_columns() {
+  static const std::vector<CsvColumn> cols = {
+      {"name", [](const ExperimentSpec& s, const PointResult&) { return s.name; }},
+      BB_NUM_COL("lambda", arrival_rate),
+      BB_INT_COL("k", k),
+      BB_INT_COL("B", batch_size),
+      BB_INT_COL("n_servers", n_servers),
+      {"error_model", [](const ExperimentSpec&, const PointResult& r) { return r.error_model; }},
+      BB_NUM_COL("p_e", p_error),
+      BB_INT_COL("n_requests", n_requests),
+      BB_INT_COL("replications", replications),
+      {"seed", [](const ExperimentSpec& s, const PointResult&) { return std::to_string(s.seed); }},
+      BB_NUM_COL("throughput_mean", throughput_mean),
+      BB_NUM_COL("throughput_std", throughput_std),
+      BB_NUM_COL("latency_mean", latency_mean),
+      BB_NUM_COL("latency_std", latency_std),
+      BB_NUM_COL("latency_p50", latency_p50),
+      BB_NUM_COL("latency_p99", latency_p99),
+      BB_NUM_COL("makespan_mean", makespan_mean),
+      BB_NUM_COL("server_busy_fraction", busy_fraction_mean),
+      BB_NUM_COL("analytic_throughput", analytic_throughput),
+      BB_NUM_COL("analytic_latency", analytic_latency),
+      BB_NUM_COL("analytic_cmax", analytic_max_throughput),
+  };
+  return cols;
+}
+#undef BB_NUM_COL
+#undef BB_INT_COL
+}  // namespace detail
+
+inline std::string results_csv_header_string() {
+  std::string h;
+  for (const auto& c : detail::csv_columns()) h.append(h.empty() ? "" : ",").append(c.name);
+  return h;
+}
+inline const char* results_csv_header() {
+  static const std::string h = results_csv_header_string();
+  return h.c_str();
+}
+inline void write_results_csv(const ExperimentSpec& spec, const std::vector<PointResult>& results,
+                              std::ostream& out) {
+  const auto& cols = detail::csv_columns();
+  out << results_csv_header() << '\n';
+  for (const PointResult& r : results) {
+    std::string row;
+    for (std::size_t c = 0; c < cols.size(); ++c) {
+      if (c) row += ',';
+      row += cols[c].cell(spec, r);
+    }
+    out << row << '\n';
+  }
+}
+inline void write_results_csv(const ExperimentSpec& spec, const std::vector<PointResult>& results,
+                              const std::string& path) {
+  std::ofstream f(path);
+  if (!f) throw std::runtime_error("cannot open results file for writing: " + path);
+  write_results_csv(spec, results, f);
 }
 
 }  // namespace binbatch

@@ -155,9 +155,12 @@ struct Servers {
 // dispatch, simulator.hpp:256-267: a batch formed at R.t starts when a server
 // is free (FIFO: the Kiefer-Wolfowitz recursion; with one server the Lindley
 // step D = max(D, R) + S, and D is also the last completion).
+// MS selects the S-server code at compile time so that the one-server kernel
+// keeps its register budget (128 regs, 16 warps/SM).
+template <bool MS>
 __device__ __forceinline__ void dispatch(Rep& R, const Servers& sv, double S, uint32_t members) {
   double fin;
-  if (sv.S == 1) {
+  if (!MS) {
     fin = R.D = __dadd_rn(fmax(R.D, R.t), S);
   } else {
     double vmin = sv.V[0];
@@ -180,7 +183,7 @@ __device__ __forceinline__ void dispatch(Rep& R, const Servers& sv, double S, ui
 
 // One request folded into its bin; closes the batch at B members
 // (on_arrival + form_batch, simulator.hpp:187-254).
-template <int SVC, bool track>
+template <int SVC, bool track, bool MS>
 __device__ __forceinline__ void fold(Rep& R, uint64_t* __restrict__ slot, double* __restrict__ osum,
                                      uint64_t xs, uint32_t B, const SvcParams& svc,
                                      const Servers& sv) {
@@ -189,7 +192,7 @@ __device__ __forceinline__ void fold(Rep& R, uint64_t* __restrict__ slot, double
   const uint32_t cnt = (uint32_t)(s0 & kCntMask) + 1;
   if (cnt == B) {
     *slot = 0;
-    dispatch(R, sv, svc_of_key_t<SVC>(svc, km >> kCntBits), B);
+    dispatch<MS>(R, sv, svc_of_key_t<SVC>(svc, km >> kCntBits), B);
     if (track) *osum = 0.0;
   } else {
     *slot = km | cnt;
@@ -206,7 +209,7 @@ __device__ __forceinline__ void fold(Rep& R, uint64_t* __restrict__ slot, double
 #ifndef BB_GEN_UNROLL
 #define BB_GEN_UNROLL 4  // requests in flight per thread (even)
 #endif
-template <int SVC, int ERR, bool OVL, bool TRACK>
+template <int SVC, int ERR, bool OVL, bool TRACK, bool MS>
 __global__ void __launch_bounds__(kGenThreads, BB_GEN_MINB) gen_kernel(const __grid_constant__ GenLaunch L) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ uint64_t s_thr[kGenWarps][BB_MAX_BINS + 1];
@@ -290,8 +293,8 @@ __global__ void __launch_bounds__(kGenThreads, BB_GEN_MINB) gen_kernel(const __g
         if (track)
           for (uint32_t b = 0; b < k; ++b) s_osum[b * kGenThreads + tid] = 0.0;
         Rep R{0.0, 0.0, 0.0, 0.0, 0.0, 0};
-        Servers srv{P.n_servers ? P.n_servers : 1u, nullptr, 0};
-        if (srv.S > 1) {  // all servers idle at t = 0
+        Servers srv{MS && P.n_servers ? P.n_servers : 1u, nullptr, 0};
+        if (MS && srv.S > 1) {  // all servers idle at t = 0
           srv.stride = gridDim.x * blockDim.x;
           srv.V = L.srv + (size_t)blockIdx.x * blockDim.x + tid;
           for (uint32_t q = 0; q < srv.S; ++q) srv.V[(size_t)q * srv.stride] = 0.0;
@@ -361,7 +364,7 @@ __global__ void __launch_bounds__(kGenThreads, BB_GEN_MINB) gen_kernel(const __g
           for (int u = 0; u < U; ++u) {
             R.t += g[u];  // exponential inter-arrival, simulator.hpp:181
             R.asum += R.t;
-            fold<SVC, TRACK>(R, st + (pb[u] - 1) * kGenThreads + tid,
+            fold<SVC, TRACK, MS>(R, st + (pb[u] - 1) * kGenThreads + tid,
                              s_osum + (pb[u] - 1) * kGenThreads + tid, d[u].xs, B, svc, srv);
           }
           if (PIPE) {
@@ -385,7 +388,7 @@ __global__ void __launch_bounds__(kGenThreads, BB_GEN_MINB) gen_kernel(const __g
             const uint32_t p0 = bin_pred(d0.xs, e0);
             R.t += exp1_from_bits53_c(d0.xg, L.coef) * inv_lambda;
             R.asum += R.t;
-            fold<SVC, TRACK>(R, st + (p0 - 1) * kGenThreads + tid, s_osum + (p0 - 1) * kGenThreads + tid,
+            fold<SVC, TRACK, MS>(R, st + (p0 - 1) * kGenThreads + tid, s_osum + (p0 - 1) * kGenThreads + tid,
                       d0.xs, B, svc, srv);
           }
         }
@@ -396,7 +399,7 @@ __global__ void __launch_bounds__(kGenThreads, BB_GEN_MINB) gen_kernel(const __g
             const uint32_t cnt = (uint32_t)(s0 & kCntMask);
             if (!cnt) continue;
             if (flush) {  // on_drain partials at the last arrival, bin order
-              dispatch(R, srv, svc_of_key_t<SVC>(svc, s0 >> kCntBits), cnt);
+              dispatch<MS>(R, srv, svc_of_key_t<SVC>(svc, s0 >> kCntBits), cnt);
             } else {
               leftover += s_osum[b * kGenThreads + tid];
             }
@@ -548,12 +551,12 @@ __global__ void point_reduce_kernel(const double* __restrict__ rep, uint32_t n_p
 }
 
 
-template <int SVC, int ERR, bool OVL, bool TRACK>
+template <int SVC, int ERR, bool OVL, bool TRACK, bool MS = false>
 cudaError_t launch_gen(const GenLaunch& L, cudaStream_t s) {
   // packed state (+ open arrival sums without flush | + overload tables)
   const size_t per = OVL ? (8 + 16) : (TRACK ? 16 : 8);
   const size_t smem = (size_t)L.k_max * kGenThreads * per;
-  auto kern = gen_kernel<SVC, ERR, OVL, TRACK>;
+  auto kern = gen_kernel<SVC, ERR, OVL, TRACK, MS>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 0, occ = 0;
@@ -585,6 +588,8 @@ cudaError_t launch_gen(const GenLaunch& L, cudaStream_t s) {
 template <int SVC, int ERR>
 cudaError_t launch_mode(const GenLaunch& L, cudaStream_t s) {
   if (L.overload) return launch_gen<SVC, ERR, true, false>(L, s);
+  // S > 1 servers: finite rates only (validated on the host); leftover sums kept
+  if (L.s_max > 1) return launch_gen<SVC, ERR, false, true, true>(L, s);
   return L.track ? launch_gen<SVC, ERR, false, true>(L, s) : launch_gen<SVC, ERR, false, false>(L, s);
 }
 

@@ -29,3 +29,34 @@ def test_dropin_reference_unit_tests_on_gpu(tmp_path):
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "0 failed" in r.stdout
+
+
+FMT = os.path.join(ROOT, "tests", "cpp", "test_formats.cpp")
+REF_INC = "/root/reference/proj/include"
+
+
+def _json_include():
+    import glob
+    hits = glob.glob("/opt/prime-rl/.venv/lib/python3*/site-packages/include/cudnn_frontend/"
+                     "thirdparty/nlohmann")
+    return hits[0] if hits else None
+
+
+@pytest.mark.skipif(not os.path.isdir(REF_INC) or _json_include() is None,
+                    reason="reference headers only exist in the build container")
+def test_output_formats_byte_identical_to_reference(tmp_path):
+    """write_request_log / write_results_csv (simulator.hpp:359-382,
+    experiment.hpp:372-414): the same program compiled against both headers
+    prints the same bytes."""
+    ref_exe, mine_exe = str(tmp_path / "fmt_ref"), str(tmp_path / "fmt_mine")
+    r = subprocess.run(["g++", "-std=c++20", "-O1", "-DBB_AGAINST_REFERENCE", "-I", REF_INC,
+                        "-I", _json_include(), FMT, "-o", ref_exe], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    r = subprocess.run(["g++", "-std=c++20", "-O1", "-I", os.path.join(ROOT, "include"), FMT,
+                        "-o", mine_exe, "-L", LIBDIR, "-l:libbinbatch_b200.so",
+                        f"-Wl,-rpath,{LIBDIR}"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    a = subprocess.run([ref_exe], capture_output=True, check=True).stdout
+    b = subprocess.run([mine_exe], capture_output=True, check=True).stdout
+    assert a == b
+    assert a.count(b"\n") == 6 + 1 + 3
