@@ -77,7 +77,7 @@ typedef struct bb_sim_config {
   double arrival_rate;     /* requests per unit time; +INFINITY == kOverload */
   uint64_t n_requests;
   uint64_t batch_size;
-  uint64_t n_servers;      /* GPU path: 1 (multi-server is BB_EUNSUPPORTED) */
+  uint64_t n_servers;      /* S >= 1 (Philox generated mode: S > 1 needs a finite rate) */
   uint64_t seed;
   int32_t flush_partial;   /* default 1 */
   int32_t has_max_batch_wait; /* GPU path: 0 */

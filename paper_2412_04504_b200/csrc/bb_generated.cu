@@ -1,32 +1,10 @@
-// bb_generated.cu -- generated-mode Monte Carlo engine (K1 + K7 + K6 of SURVEY §2.3).
-//
-// One thread simulates one replication end to end, a warp owns 32
-// replications of one sweep point, and a persistent grid walks the
-// (point, 32-replication chunk) work list.  Per request the thread draws one
-// Philox4x32-10 block (53-bit inter-arrival uniform + 53-bit service key),
-// assigns the bin in key space, folds the request into its bin's packed
-// (max key, count) word in shared memory and, when the bin reaches B, closes
-// the batch with the single-server Lindley step
-//     D = max(D, R) + S,  R = arrival of the closing request
-// (simulator.hpp:256-267 with one server).  Nothing per request
-// touches HBM: the kernel is SM-issue bound.
-//
-// Dispatch semantics reproduced:
-//   finite lambda -- batches dispatch in closing-request order, then the
-//     final partials in bin order 1..k (drain events, simulator.hpp:203-205);
-//   overload -- one tie group: round 0 in first-closing order, then either
-//     round-robin rounds (no flush) or per-bin drains (flush).  Positions are
-//     closed-form from a first counting pass; the second pass replays the
-//     same counter-based draws.
+// bb_generated.cu -- generated-mode host entry points: key-space threshold
+// setup, the per-family kernel dispatch (bb_gen_kernel.cuh) and the
+// per-point replica reduction.
 #include "bb_generated.cuh"
 
 namespace bb {
 namespace {
-
-constexpr int kGenThreads = 256;
-constexpr int kGenWarps = kGenThreads / 32;
-constexpr uint64_t kCntBits = 11;
-constexpr uint64_t kCntMask = (1ull << kCntBits) - 1;  // B <= 2047 in the packed state
 
 __global__ void thresholds_kernel(GenPoint* pts, uint32_t n_points) {
   const uint32_t p = blockIdx.x;
@@ -87,440 +65,6 @@ __global__ void thresholds_kernel(GenPoint* pts, uint32_t n_points) {
   }
 }
 
-// 1 + #{j in 1..k-1 : thr[j] <= x}  (== assign_bin for monotone s(x))
-__device__ __forceinline__ uint32_t bin_of(const uint64_t* thr, const uint8_t* lut, bool lut_ok,
-                                           uint32_t k, uint32_t top, uint64_t x) {
-  if (lut_ok) {  // one table read + at most one threshold compare
-    const uint32_t c = lut[x >> 45];
-    return c + 1 + (c + 1 < k && thr[c + 1] <= x);
-  }
-  uint32_t pos = 0;
-  for (uint32_t step = top; step; step >>= 1)
-    if (pos + step < k && thr[pos + step] <= x) pos += step;
-  return pos + 1;
-}
-
-// predict_bin, binning.hpp:231-261, in key space of the error uniform
-template <int ERR>
-__device__ __forceinline__ uint32_t predict(const GenPoint& P, uint32_t tb, uint32_t k,
-                                            uint64_t xe) {
-  if (ERR == 1) {
-    if (tb == 1) return xe < P.e_t1 ? 2u : 1u;
-    if (tb == k) return xe < P.e_t1 ? k - 1 : k;
-    if (xe < P.e_t1) return tb - 1;
-    if (xe >= P.e_t2) return tb + 1;
-    return tb;
-  } else if (ERR == 2) {
-    const uint64_t* row = P.conf_thr + (uint64_t)(tb - 1) * k;
-    uint32_t pb = 1;
-    for (uint32_t j = 0; j + 1 < k; ++j) pb += xe >= row[j];
-    return pb;
-  }
-  return tb;
-}
-
-struct Draw {
-  uint64_t xg;  // inter-arrival uniform (53-bit)
-  uint64_t xs;  // service key
-};
-
-template <int SVC>
-__device__ __forceinline__ Draw draw(const uint32_t* __restrict__ cyc_rank, uint32_t n_table,
-                                     uint32_t i, uint32_t c2, uint32_t c3, uint32_t& cyc) {
-  Draw d;
-  const uint4 r = philox(i, kStreamArrivalService, c2, c3);
-  d.xg = bits53(r.x, r.y);
-  if (SVC == kSvcCyclic) {
-    d.xs = cyc_rank[cyc];
-    if (++cyc == n_table) cyc = 0;
-  } else {
-    d.xs = bits53(r.z, r.w);
-  }
-  return d;
-}
-
-// Per-replication state of the finite-rate simulation (registers).
-struct Rep {
-  double t, D, busy, latw, asum;
-  uint64_t ncomp;
-};
-
-// S servers' free times (multi-server runs only), strided per thread.
-struct Servers {
-  uint32_t S;
-  double* V;
-  uint32_t stride;
-};
-
-// dispatch, simulator.hpp:256-267: a batch formed at R.t starts when a server
-// is free (FIFO: the Kiefer-Wolfowitz recursion; with one server the Lindley
-// step D = max(D, R) + S, and D is also the last completion).
-// MS selects the S-server code at compile time so that the one-server kernel
-// keeps its register budget (128 regs, 16 warps/SM).
-template <bool MS>
-__device__ __forceinline__ void dispatch(Rep& R, const Servers& sv, double S, uint32_t members) {
-  double fin;
-  if (!MS) {
-    fin = R.D = __dadd_rn(fmax(R.D, R.t), S);
-  } else {
-    double vmin = sv.V[0];
-    uint32_t im = 0;
-    for (uint32_t q = 1; q < sv.S; ++q) {
-      const double v = sv.V[(size_t)q * sv.stride];
-      if (v < vmin) {
-        vmin = v;
-        im = q;
-      }
-    }
-    fin = __dadd_rn(fmax(vmin, R.t), S);
-    sv.V[(size_t)im * sv.stride] = fin;
-    R.D = fmax(R.D, fin);  // last completion (simulator.hpp:275)
-  }
-  R.busy += S;
-  R.latw += (double)members * fin;
-  R.ncomp += members;
-}
-
-// One request folded into its bin; closes the batch at B members
-// (on_arrival + form_batch, simulator.hpp:187-254).
-template <int SVC, bool track, bool MS>
-__device__ __forceinline__ void fold(Rep& R, uint64_t* __restrict__ slot, double* __restrict__ osum,
-                                     uint64_t xs, uint32_t B, const SvcParams& svc,
-                                     const Servers& sv) {
-  const uint64_t s0 = *slot;
-  const uint64_t km = max(s0 & ~kCntMask, xs << kCntBits);
-  const uint32_t cnt = (uint32_t)(s0 & kCntMask) + 1;
-  if (cnt == B) {
-    *slot = 0;
-    dispatch<MS>(R, sv, svc_of_key_t<SVC>(svc, km >> kCntBits), B);
-    if (track) *osum = 0.0;
-  } else {
-    *slot = km | cnt;
-    if (track) *osum += R.t;
-  }
-}
-
-#ifndef BB_GEN_MINB
-#define BB_GEN_MINB 1
-#endif
-#ifndef BB_GEN_PIPE
-#define BB_GEN_PIPE 0  // software-pipeline the next group's draws (A/B: slower, 134 regs)
-#endif
-#ifndef BB_GEN_UNROLL
-#define BB_GEN_UNROLL 4  // requests in flight per thread (even)
-#endif
-template <int SVC, int ERR, bool OVL, bool TRACK, bool MS>
-__global__ void __launch_bounds__(kGenThreads, BB_GEN_MINB) gen_kernel(const __grid_constant__ GenLaunch L) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  __shared__ uint64_t s_thr[kGenWarps][BB_MAX_BINS + 1];
-  __shared__ __align__(16) uint8_t s_lut[kGenWarps][256];
-  const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5, tid = threadIdx.x;
-  const uint32_t kmax = L.k_max;
-  uint64_t* st = reinterpret_cast<uint64_t*>(smem_raw);  // [kmax][T] packed (key<<11 | cnt)
-  double* s_osum = reinterpret_cast<double*>(st + (size_t)kmax * kGenThreads);  // finite, no flush
-  uint32_t* s_F = reinterpret_cast<uint32_t*>(st + (size_t)kmax * kGenThreads);  // overload
-  uint32_t* s_rem = s_F + (size_t)kmax * kGenThreads;
-  uint32_t* s_cf = s_rem + (size_t)kmax * kGenThreads;
-  uint32_t* s_jd = s_cf + (size_t)kmax * kGenThreads;
-
-  const uint32_t nrep = L.rep_end - L.rep_begin;
-  const uint32_t chunks = (nrep + 31) / 32;
-  const uint64_t n_items = (uint64_t)chunks * L.n_points;
-  const uint64_t stride = (uint64_t)L.points_total * L.reps_total;
-  const uint64_t gwarp = (uint64_t)blockIdx.x * kGenWarps + wib;
-  const uint64_t nwarps = (uint64_t)gridDim.x * kGenWarps;
-
-  for (uint64_t w = gwarp; w < n_items; w += nwarps) {
-    const uint32_t p = (uint32_t)(w / chunks), c = (uint32_t)(w % chunks);
-    const GenPoint& P = L.pts_dev[p];
-    const uint32_t k = P.k, B = P.B, n = P.n;
-    for (uint32_t j = lane; j <= k; j += 32) s_thr[wib][j] = P.thr[j];
-    reinterpret_cast<uint2*>(s_lut[wib])[lane] = reinterpret_cast<const uint2*>(P.lut)[lane];
-    __syncwarp();
-    const uint32_t r = L.rep_begin + c * 32 + lane;
-    if (r < L.rep_end) {
-      const uint64_t seed = L.single_seed ? L.master : replication_seed(L.master, r);
-      const uint64_t sw = splitmix64(seed);  // RandomStream(seed) whitening, rng.hpp:30
-      const uint32_t c2 = (uint32_t)sw, c3 = (uint32_t)(sw >> 32);
-      // point parameters in registers (the closures read them, not global memory)
-      const SvcParams svc = P.svc;
-      const uint32_t* __restrict__ cyc_rank = P.cyc_rank;
-      const uint64_t* __restrict__ conf_thr = P.conf_thr;
-      const uint64_t* thr = s_thr[wib];
-      const uint8_t* lut = s_lut[wib];
-      const bool lut_ok = P.lut_ok != 0;
-      const uint32_t top = k > 1 ? (1u << (31 - __clz(k - 1))) : 0u;
-      const bool check = P.check_domain != 0;
-      const uint64_t vlo = P.vlo, vhi = P.vhi, et1 = P.e_t1, et2 = P.e_t2;
-      const bool flush = P.flush != 0;
-      const uint32_t nt = svc.n_table;
-      for (uint32_t b = 0; b < k; ++b) st[b * kGenThreads + tid] = 0;
-      uint32_t cyc = 0;
-      bool failed = false;
-      double thr_out, lat_out, mk_out, busy_out;
-
-      // bin of a key, then the error model (predict_bin, binning.hpp:231-261)
-      auto bin_pred = [&](uint64_t xs, uint64_t xe) -> uint32_t {
-        const uint32_t tb = k > 1 ? bin_of(thr, lut, lut_ok, k, top, xs) : 1u;
-        if (ERR == 1) {
-          if (tb == 1) return xe < et1 ? 2u : 1u;
-          if (tb == k) return xe < et1 ? k - 1 : k;
-          if (xe < et1) return tb - 1;
-          if (xe >= et2) return tb + 1;
-          return tb;
-        } else if (ERR == 2) {
-          const uint64_t* row = conf_thr + (uint64_t)(tb - 1) * k;
-          uint32_t pb = 1;
-          for (uint32_t j = 0; j + 1 < k; ++j) pb += xe >= row[j];
-          return pb;
-        }
-        return tb;
-      };
-      // the error stream's two uniforms for requests (2m, 2m+1)
-      auto err_pair = [&](uint32_t i, uint64_t& e0, uint64_t& e1) {
-        if (ERR != 0) {
-          const uint4 e = philox(i >> 1, kStreamError, c2, c3);
-          e0 = bits53(e.x, e.y);
-          e1 = bits53(e.z, e.w);
-        }
-      };
-      auto out_of_support = [&](uint64_t xs) { return check && (xs < vlo || xs > vhi); };
-
-      if (!OVL) {
-        // ------------------------------------------------ finite arrival rate
-        const double inv_lambda = P.inv_lambda;
-        constexpr bool track = TRACK;  // no flush at a finite rate: leftover sums needed
-        if (track)
-          for (uint32_t b = 0; b < k; ++b) s_osum[b * kGenThreads + tid] = 0.0;
-        Rep R{0.0, 0.0, 0.0, 0.0, 0.0, 0};
-        Servers srv{MS && P.n_servers ? P.n_servers : 1u, nullptr, 0};
-        if (MS && srv.S > 1) {  // all servers idle at t = 0
-          srv.stride = gridDim.x * blockDim.x;
-          srv.V = L.srv + (size_t)blockIdx.x * blockDim.x + tid;
-          for (uint32_t q = 0; q < srv.S; ++q) srv.V[(size_t)q * srv.stride] = 0.0;
-        }
-        uint32_t cyc0 = 0;
-        const double a0 = exp1_from_bits53_c(draw<SVC>(cyc_rank, nt, 0, c2, c3, cyc0).xg, L.coef) * inv_lambda;
-        // U requests per iteration: their draws, exponentials and bins are
-        // independent, so the latencies overlap; the folds stay in order
-        constexpr int U = BB_GEN_UNROLL;
-        // software pipeline: the next group's Philox blocks (integer pipes)
-        // are issued in the same basic block as this group's exponentials
-        // (fp64 pipe) so the scheduler interleaves them (cyclic traces keep a
-        // running table index and are not pipelined)
-        constexpr bool PIPE = BB_GEN_PIPE && SVC != kSvcCyclic;
-        uint32_t i = 0;
-        Draw d[U];
-        uint64_t e[U];
-        if (PIPE && U <= n) {
-#pragma unroll
-          for (int u = 0; u < U; ++u) d[u] = draw<SVC>(cyc_rank, nt, u, c2, c3, cyc);
-#pragma unroll
-          for (int u = 0; u < U; u += 2) {
-            e[u] = e[u + 1] = 0;
-            err_pair(u, e[u], e[u + 1]);
-          }
-        }
-        for (; i + U <= n; i += U) {
-          double g[U];
-          uint32_t pb[U];
-          Draw dn[U];
-          uint64_t en[U];
-          if (!PIPE) {
-#pragma unroll
-            for (int u = 0; u < U; ++u) d[u] = draw<SVC>(cyc_rank, nt, i + u, c2, c3, cyc);
-#pragma unroll
-            for (int u = 0; u < U; u += 2) {
-              e[u] = e[u + 1] = 0;
-              err_pair(i + u, e[u], e[u + 1]);
-            }
-          } else {
-#pragma unroll
-            for (int u = 0; u < U; ++u) dn[u] = draw<SVC>(cyc_rank, nt, i + U + u, c2, c3, cyc);
-#pragma unroll
-            for (int u = 0; u < U; u += 2) {
-              en[u] = en[u + 1] = 0;
-              err_pair(i + U + u, en[u], en[u + 1]);
-            }
-          }
-#pragma unroll
-          for (int u = 0; u < U; ++u) g[u] = exp1_from_bits53_c(d[u].xg, L.coef) * inv_lambda;
-          bool oos = false;
-#pragma unroll
-          for (int u = 0; u < U; ++u) oos |= out_of_support(d[u].xs);
-          if (oos) {  // first offending request (no dynamic indexing: keeps d[] in registers)
-            uint32_t bad = 0;
-            uint64_t bx = 0;
-#pragma unroll
-            for (int u = U - 1; u >= 0; --u)
-              if (out_of_support(d[u].xs)) bad = (uint32_t)u, bx = d[u].xs;
-            raise_error(L.err, i + bad, BB_EDOMAIN, svc_of_key_t<SVC>(svc, bx), r);
-            failed = true;
-            break;
-          }
-#pragma unroll
-          for (int u = 0; u < U; ++u) pb[u] = bin_pred(d[u].xs, e[u]);
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            R.t += g[u];  // exponential inter-arrival, simulator.hpp:181
-            R.asum += R.t;
-            fold<SVC, TRACK, MS>(R, st + (pb[u] - 1) * kGenThreads + tid,
-                             s_osum + (pb[u] - 1) * kGenThreads + tid, d[u].xs, B, svc, srv);
-          }
-          if (PIPE) {
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-              d[u] = dn[u];
-              e[u] = en[u];
-            }
-          }
-        }
-        // tail: fewer than U requests left, one at a time
-        for (; !failed && i < n; ++i) {
-          const Draw d0 = draw<SVC>(cyc_rank, nt, i, c2, c3, cyc);
-          uint64_t e0 = 0, e1 = 0;
-          err_pair(i & ~1u, e0, e1);
-          if (i & 1u) e0 = e1;
-          if (out_of_support(d0.xs)) {
-            raise_error(L.err, i, BB_EDOMAIN, svc_of_key_t<SVC>(svc, d0.xs), r);
-            failed = true;
-          } else {
-            const uint32_t p0 = bin_pred(d0.xs, e0);
-            R.t += exp1_from_bits53_c(d0.xg, L.coef) * inv_lambda;
-            R.asum += R.t;
-            fold<SVC, TRACK, MS>(R, st + (p0 - 1) * kGenThreads + tid, s_osum + (p0 - 1) * kGenThreads + tid,
-                      d0.xs, B, svc, srv);
-          }
-        }
-        double leftover = 0.0;
-        if (!failed) {
-          for (uint32_t b = 0; b < k; ++b) {
-            const uint64_t s0 = st[b * kGenThreads + tid];
-            const uint32_t cnt = (uint32_t)(s0 & kCntMask);
-            if (!cnt) continue;
-            if (flush) {  // on_drain partials at the last arrival, bin order
-              dispatch<MS>(R, srv, svc_of_key_t<SVC>(svc, s0 >> kCntBits), cnt);
-            } else {
-              leftover += s_osum[b * kGenThreads + tid];
-            }
-          }
-        }
-        if (!failed && R.ncomp > 0) {  // finish(), simulator.hpp:279-301
-          mk_out = R.D - a0;
-          thr_out = (double)R.ncomp / mk_out;
-          busy_out = R.busy / ((double)srv.S * mk_out);  // simulator.hpp:287-288
-          lat_out = (R.latw - (R.asum - leftover)) / (double)R.ncomp;
-        } else {
-          mk_out = thr_out = busy_out = lat_out = failed ? BB_QNAN : 0.0;
-        }
-      } else {
-        // ------------------------------------------------------- overload
-        for (uint32_t b = 0; b < k; ++b) {
-          s_F[b * kGenThreads + tid] = 0;
-          s_cf[b * kGenThreads + tid] = 0xFFFFFFFFu;
-        }
-        uint64_t e0 = 0, e1 = 0;
-        for (uint32_t i = 0; i < n; ++i) {  // pass 1: per-bin totals, first closings
-          const Draw d = draw<SVC>(cyc_rank, nt, i, c2, c3, cyc);
-          if ((i & 1u) == 0) err_pair(i, e0, e1);
-          if (out_of_support(d.xs)) {
-            raise_error(L.err, i, BB_EDOMAIN, svc_of_key_t<SVC>(svc, d.xs), r);
-            failed = true;
-            break;
-          }
-          const uint32_t pb = bin_pred(d.xs, (i & 1u) ? e1 : e0);
-          const uint32_t cnt = ++s_F[(pb - 1) * kGenThreads + tid];
-          if (cnt == B) s_cf[(pb - 1) * kGenThreads + tid] = i;
-        }
-        if (!failed) {
-          uint32_t Z = 0;
-          uint64_t nc = 0;
-          for (uint32_t b = 0; b < k; ++b) {
-            const uint32_t cnt = s_F[b * kGenThreads + tid];
-            const uint32_t F = cnt / B, rem = cnt - F * B;
-            s_F[b * kGenThreads + tid] = F;
-            s_rem[b * kGenThreads + tid] = rem;
-            s_jd[b * kGenThreads + tid] = 0;
-            Z += F >= 1;
-            nc += (uint64_t)F * B + (flush ? rem : 0);
-          }
-          cyc = 0;
-          double busy = 0.0, latw = 0.0;
-          for (uint32_t i = 0; i < n; ++i) {  // pass 2: same draws, batch positions
-            const Draw d = draw<SVC>(cyc_rank, nt, i, c2, c3, cyc);
-            if ((i & 1u) == 0) err_pair(i, e0, e1);
-            const uint32_t pb = bin_pred(d.xs, (i & 1u) ? e1 : e0);
-            uint64_t* slot = st + (pb - 1) * kGenThreads + tid;
-            const uint64_t s0 = *slot;
-            const uint64_t km = max(s0 & ~kCntMask, d.xs << kCntBits);
-            const uint32_t cnt = (uint32_t)(s0 & kCntMask) + 1;
-            if (cnt == B) {
-              *slot = 0;
-              const uint32_t b = pb - 1;
-              const uint32_t j = s_jd[b * kGenThreads + tid]++;
-              const uint32_t cfb = s_cf[b * kGenThreads + tid];
-              uint64_t before;
-              if (flush && j > 0) {  // drain phase, bins in order (on_drain, :218-221)
-                before = (uint64_t)B * Z + (uint64_t)B * (j - 1);
-                for (uint32_t q = 0; q < b; ++q) {
-                  const uint32_t F = s_F[q * kGenThreads + tid];
-                  before += (uint64_t)B * (F ? F - 1 : 0) + s_rem[q * kGenThreads + tid];
-                }
-              } else {  // round j, first-closing order (on_formation, :208-216)
-                uint64_t pos = 0;
-                for (uint32_t q = 0; q < k; ++q) {
-                  const uint32_t F = s_F[q * kGenThreads + tid];
-                  const uint32_t cq = s_cf[q * kGenThreads + tid];
-                  if (!flush) pos += F < j ? F : j;
-                  pos += (cq < cfb) && (F > j);
-                }
-                before = (uint64_t)B * pos;
-              }
-              const double S = svc_of_key_t<SVC>(svc, km >> kCntBits);
-              busy += S;
-              latw += S * (double)(nc - before);
-            } else {
-              *slot = km | cnt;
-            }
-          }
-          if (flush) {
-            uint64_t base = (uint64_t)B * Z;
-            for (uint32_t b = 0; b < k; ++b) {
-              const uint32_t F = s_F[b * kGenThreads + tid];
-              const uint32_t rem = s_rem[b * kGenThreads + tid];
-              base += (uint64_t)B * (F ? F - 1 : 0);
-              if (rem) {
-                const double S = svc_of_key_t<SVC>(svc, st[b * kGenThreads + tid] >> kCntBits);
-                busy += S;
-                latw += S * (double)(nc - base);
-              }
-              base += rem;
-            }
-          }
-          if (nc > 0) {
-            mk_out = busy;  // all requests arrive at t=0 and the server never idles
-            thr_out = (double)nc / mk_out;
-            busy_out = busy / mk_out;
-            lat_out = latw / (double)nc;
-          } else {
-            mk_out = thr_out = busy_out = lat_out = 0.0;
-          }
-        } else {
-          mk_out = thr_out = busy_out = lat_out = BB_QNAN;
-        }
-      }
-      const uint64_t o = (uint64_t)P.gidx * L.reps_total + r;
-      L.out[BB_REP_THROUGHPUT * stride + o] = thr_out;
-      L.out[BB_REP_LATENCY * stride + o] = lat_out;
-      L.out[BB_REP_P50 * stride + o] = BB_QNAN;  // generated mode: not tracked (SURVEY §7 hard part 4)
-      L.out[BB_REP_P99 * stride + o] = BB_QNAN;
-      L.out[BB_REP_MAKESPAN * stride + o] = mk_out;
-      L.out[BB_REP_BUSY * stride + o] = busy_out;
-    }
-    __syncwarp();
-  }
-}
-
 // mean_std (experiment.hpp:188-200) in replica order, bit-for-bit the
 // reference's sequential sums.  One block per point, one thread per field.
 __global__ void point_reduce_kernel(const double* __restrict__ rep, uint32_t n_points,
@@ -550,59 +94,6 @@ __global__ void point_reduce_kernel(const double* __restrict__ rep, uint32_t n_p
   }
 }
 
-
-template <int SVC, int ERR, bool OVL, bool TRACK, bool MS = false>
-cudaError_t launch_gen(const GenLaunch& L, cudaStream_t s) {
-  // packed state (+ open arrival sums without flush | + overload tables)
-  const size_t per = OVL ? (8 + 16) : (TRACK ? 16 : 8);
-  const size_t smem = (size_t)L.k_max * kGenThreads * per;
-  auto kern = gen_kernel<SVC, ERR, OVL, TRACK, MS>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  int dev = 0, sms = 0, occ = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kGenThreads, smem);
-  if (e != cudaSuccess) return e;
-  if (occ < 1) return cudaErrorInvalidConfiguration;
-  const uint32_t nrep = L.rep_end - L.rep_begin;
-  const uint64_t items = (uint64_t)((nrep + 31) / 32) * L.n_points;
-  const uint64_t want = (items + kGenWarps - 1) / kGenWarps;
-  const uint64_t cap = (uint64_t)sms * occ;
-  const unsigned grid = (unsigned)(want < cap ? want : cap);
-  if (grid == 0) return cudaSuccess;
-  GenLaunch L2 = L;
-  double* srv = nullptr;
-  if (L.s_max > 1) {  // free times of S servers per resident thread
-    e = cudaMallocAsync((void**)&srv, (size_t)grid * kGenThreads * L.s_max * sizeof(double), s);
-    if (e != cudaSuccess) return e;
-    L2.srv = srv;
-  }
-  kern<<<grid, kGenThreads, smem, s>>>(L2);
-  note_launch();
-  e = cudaGetLastError();
-  if (srv) cudaFreeAsync(srv, s);
-  return e;
-}
-
-template <int SVC, int ERR>
-cudaError_t launch_mode(const GenLaunch& L, cudaStream_t s) {
-  if (L.overload) return launch_gen<SVC, ERR, true, false>(L, s);
-  // S > 1 servers: finite rates only (validated on the host); leftover sums kept
-  if (L.s_max > 1) return launch_gen<SVC, ERR, false, true, true>(L, s);
-  return L.track ? launch_gen<SVC, ERR, false, true>(L, s) : launch_gen<SVC, ERR, false, false>(L, s);
-}
-
-template <int SVC>
-cudaError_t launch_svc(const GenLaunch& L, cudaStream_t s) {
-  switch (L.err_kind) {
-    case 0: return launch_mode<SVC, 0>(L, s);
-    case 1: return launch_mode<SVC, 1>(L, s);
-    case 2: return launch_mode<SVC, 2>(L, s);
-  }
-  return cudaErrorInvalidValue;
-}
-
 }  // namespace
 
 cudaError_t gen_setup_thresholds(GenPoint* pts_dev, uint32_t n_points, cudaStream_t s) {
@@ -616,12 +107,12 @@ cudaError_t gen_run(const GenLaunch& L0, cudaStream_t s) {
   GenLaunch L = L0;
   L.coef = make_atanh_coef();
   switch (L.svc_kind) {
-    case kSvcUniform: return launch_svc<kSvcUniform>(L, s);
-    case kSvcLinear: return launch_svc<kSvcLinear>(L, s);
-    case kSvcExponential: return launch_svc<kSvcExponential>(L, s);
-    case kSvcLogNormal: return launch_svc<kSvcLogNormal>(L, s);
-    case kSvcTable: return launch_svc<kSvcTable>(L, s);
-    case kSvcCyclic: return launch_svc<kSvcCyclic>(L, s);
+    case kSvcUniform: return gen_run_svc<kSvcUniform>(L, s);
+    case kSvcLinear: return gen_run_svc<kSvcLinear>(L, s);
+    case kSvcExponential: return gen_run_svc<kSvcExponential>(L, s);
+    case kSvcLogNormal: return gen_run_svc<kSvcLogNormal>(L, s);
+    case kSvcTable: return gen_run_svc<kSvcTable>(L, s);
+    case kSvcCyclic: return gen_run_svc<kSvcCyclic>(L, s);
   }
   return cudaErrorInvalidValue;
 }

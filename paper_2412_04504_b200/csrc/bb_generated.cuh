@@ -45,11 +45,17 @@ struct GenLaunch {
   AtanhCoef coef;           // exponential-variate polynomial (param space)
   uint32_t s_max;           // largest n_servers in the launch
   double* srv;              // server free times scratch (set by gen_run)
+  uint32_t nb_max;          // overload, S > 1: most batches of any point (n/B + k)
+  double* ovS;              // overload, S > 1: per-thread batch services (set by gen_run)
+  uint16_t* ovM;            //   ... and member counts
   DevError* err;
 };
 
 // Resolves key-space thresholds (bisection on the device sampler).
 cudaError_t gen_setup_thresholds(GenPoint* pts_dev, uint32_t n_points, cudaStream_t s);
+// The fused per-replica kernel of one service family (bb_gen_<family>.cu).
+template <int SVC>
+cudaError_t gen_run_svc(const GenLaunch& L, cudaStream_t s);
 // The fused per-replica kernel.  Returns the launch error.
 cudaError_t gen_run(const GenLaunch& L, cudaStream_t s);
 // mean_std per point over replica order (experiment.hpp:188-200, :275-281).

@@ -396,7 +396,7 @@ SimSpec make_spec(const bb_sim_config* c, bool single = true) {
   s.rng = c->rng;
   if (!single) return s;
   // the GPU envelope (SURVEY §8f lists these as the next rows)
-  if (c->n_servers != 1) raise(BB_EUNSUPPORTED, "n_servers > 1 is not implemented on the GPU path yet");
+  if (c->n_servers >= (1ull << 32)) raise(BB_EUNSUPPORTED, "n_servers must be < 2^32");
   if (c->has_max_batch_wait) raise(BB_EUNSUPPORTED, "max_batch_wait is not implemented on the GPU path yet");
   if (k > BB_TRACE_MAX_BINS) raise(BB_EUNSUPPORTED, "more than 32 bins is not supported for single runs");
   if (c->n_requests >= (1ull << 32) - 1) raise(BB_EUNSUPPORTED, "n_requests must be < 2^32");
@@ -593,6 +593,7 @@ void run_pipeline(const SimSpec& c, const double* a_dev, const double* s_dev, co
   A.n = (uint32_t)n;
   A.B = (uint32_t)c.B;
   A.k = (uint32_t)k;
+  A.n_servers = (uint32_t)c.S;
   A.flush = c.flush;
   A.err_kind = pred_dev ? 0 : (c.error_draws() ? c.err_kind : 0);
   A.p_error = c.p;
@@ -863,7 +864,9 @@ struct SweepParams {
   uint64_t seed, replications;
 };
 
-void build_sweep(std::vector<bb_run_template> tpl, Sweep& W, cudaStream_t st) {
+// `generated`: the points run in the fused Philox kernel (its envelope is
+// checked); reference-stream points run the trace pipeline per replication.
+void build_sweep(std::vector<bb_run_template> tpl, Sweep& W, cudaStream_t st, bool generated = true) {
   if (tpl.empty()) raise(BB_EINVAL, "sweep has no points");
   W.tpl = std::move(tpl);
   const size_t P = W.tpl.size();
@@ -871,10 +874,9 @@ void build_sweep(std::vector<bb_run_template> tpl, Sweep& W, cudaStream_t st) {
   for (auto& t : W.tpl) {
     W.spec.push_back(materialize(t, 0));
     const SimSpec& s = W.spec.back();
-    if (s.S != 1 && std::isinf(s.lambda))
-      raise(BB_EUNSUPPORTED, "n_servers > 1 at overload is not implemented on the GPU path yet");
-    if (s.S > 4096) raise(BB_EUNSUPPORTED, "more than 4096 servers is not supported");
     if (t.has_max_batch_wait) raise(BB_EUNSUPPORTED, "max_batch_wait is not implemented on the GPU path yet");
+    if (!generated) continue;
+    if (s.S > 4096) raise(BB_EUNSUPPORTED, "more than 4096 servers is not supported");
     if (s.k() > BB_MAX_BINS) raise(BB_EUNSUPPORTED, "more than 64 bins is not supported");
     if (s.B > 2047) raise(BB_EUNSUPPORTED, "batch sizes above 2047 are not supported by the fused kernel");
     if (s.n >= (1ull << 32) - 1) raise(BB_EUNSUPPORTED, "n_requests must be < 2^32");
@@ -939,25 +941,28 @@ void launch_sweep(const SweepParams* E, Sweep& W, uint64_t rep_begin, uint64_t r
   // group points by kernel instantiation; each group's points are copied
   // (already threshold-resolved) into a contiguous device array
   struct Key {
-    int err, cyc, ovl, track;
+    int err, cyc, ovl, track, ms;
   };
   std::vector<Key> keys(P);
   for (size_t i = 0; i < P; ++i)
     keys[i] = Key{(int)W.gp[i].err_kind, (int)W.gp[i].svc.kind, W.gp[i].inv_lambda == 0.0,
-                  W.gp[i].inv_lambda != 0.0 && !W.gp[i].flush};
+                  W.gp[i].inv_lambda != 0.0 && !W.gp[i].flush, W.gp[i].n_servers > 1};
   std::vector<bool> done(P, false);
   bool first = true;
   for (size_t i = 0; i < P; ++i) {
     if (done[i]) continue;
     std::vector<uint32_t> members;
     uint32_t kmax = 1, smax = 1;
+    uint64_t nbmax = 1;
     for (size_t j = i; j < P; ++j)
       if (!done[j] && keys[j].err == keys[i].err && keys[j].cyc == keys[i].cyc &&
-          keys[j].ovl == keys[i].ovl && keys[j].track == keys[i].track) {
+          keys[j].ovl == keys[i].ovl && keys[j].track == keys[i].track &&
+          keys[j].ms == keys[i].ms) {
         members.push_back((uint32_t)j);
         done[j] = true;
         kmax = std::max(kmax, W.gp[j].k);
         smax = std::max(smax, W.gp[j].n_servers);
+        nbmax = std::max<uint64_t>(nbmax, W.gp[j].n / W.gp[j].B + W.gp[j].k + 1);
       }
     const bb::GenPoint* base = W.d_pts.as<bb::GenPoint>();
     DBuf grp;
@@ -977,6 +982,7 @@ void launch_sweep(const SweepParams* E, Sweep& W, uint64_t rep_begin, uint64_t r
     L.points_total = (uint32_t)P;
     L.k_max = kmax;
     L.s_max = smax;
+    L.nb_max = (uint32_t)nbmax;
     L.master = E->seed;
     L.single_seed = 0;
     L.reps_total = (uint32_t)E->replications;
@@ -1075,7 +1081,7 @@ void reference_point_reps(const SweepParams* E, const Sweep& W, std::vector<doub
   rep.assign(BB_REP_FIELDS * P * R, 0.0);
   for (size_t i = 0; i < P; ++i) {
     SimSpec s = W.spec[i];
-    if (s.S != 1) raise(BB_EUNSUPPORTED, "n_servers > 1 in reference-stream mode is not implemented yet");
+    if (s.S >= (1ull << 32)) raise(BB_EUNSUPPORTED, "n_servers must be < 2^32");
     if (s.k() > BB_TRACE_MAX_BINS) raise(BB_EUNSUPPORTED, "more than 32 bins in reference-stream mode");
     for (uint64_t r = 0; r < R; ++r) {
       s.seed = bb::replication_seed(E->seed, r);
@@ -1103,7 +1109,7 @@ void run_points_host(std::vector<bb_run_template> tpl, SweepParams E, int32_t rn
   std::lock_guard<std::mutex> lock(g_ctx[dev].mu);
   cudaStream_t st = ctx_stream(dev);
   Sweep W;
-  build_sweep(std::move(tpl), W, st);
+  build_sweep(std::move(tpl), W, st, rng != BB_RNG_REFERENCE);
   const uint64_t P = W.tpl.size(), R = E.replications;
   DBuf rep(BB_REP_FIELDS * P * R * 8, st), stats(P * 8 * 8, st);
   if (rng == BB_RNG_REFERENCE) {

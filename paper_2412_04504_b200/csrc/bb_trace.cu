@@ -1031,6 +1031,70 @@ struct QArgs {
   uint32_t* members;
 };
 
+// ------------------------------------------------ multi-server dispatch
+// S > 1 servers (simulator.hpp:256-277): the central queue is FIFO, so batch
+// i starts on the earliest-free server, start_i = max(R_i, min_j V_j), and
+// that server's free time becomes finish_i = fl(start_i + S_i) (the
+// Kiefer-Wolfowitz recursion; a server freed at R_i is idle for a batch
+// formed at R_i because batch_done events rank first, :108-114).  One block:
+// all threads stage chunks of (R, S) in shared memory, thread 0 runs the
+// recursion over a binary min-heap of free times (shared memory up to
+// KW_HEAP servers), the block writes (start, finish) back.  busy_time_ and
+// last_completion_ accumulate in dispatch order, as the reference does.
+constexpr uint32_t KW_CH = 1024, KW_HEAP = 2048;
+__global__ void __launch_bounds__(256) kw_dispatch_kernel(const double* __restrict__ R,
+                                                          const double* __restrict__ S, uint32_t nb,
+                                                          uint32_t nsrv, double* heap_g,
+                                                          double* __restrict__ start,
+                                                          double* __restrict__ finish,
+                                                          double* busy_out, double* last_out) {
+  __shared__ double sA[KW_CH], sB[KW_CH];  // (R, S) in, (start, finish) out
+  __shared__ double sheap[KW_HEAP];
+  double* heap = nsrv <= KW_HEAP ? sheap : heap_g;
+  for (uint32_t i = threadIdx.x; i < nsrv; i += blockDim.x) heap[i] = -CUDART_INF;  // all idle
+  double busy = 0.0, last = 0.0;
+  for (uint32_t base = 0; base < nb; base += KW_CH) {
+    const uint32_t m = min(KW_CH, nb - base);
+    __syncthreads();
+    for (uint32_t j = threadIdx.x; j < m; j += blockDim.x) {
+      sA[j] = R[base + j];
+      sB[j] = S[base + j];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (uint32_t j = 0; j < m; ++j) {
+        const double sv = sB[j];
+        const double st = fmax(heap[0], sA[j]);
+        const double f = __dadd_rn(st, sv);
+        sA[j] = st;
+        sB[j] = f;
+        busy = __dadd_rn(busy, sv);
+        last = fmax(last, f);
+        // replace the minimum by f (f >= old minimum) and sift down
+        uint32_t h = 0;
+        for (;;) {
+          uint32_t c = 2 * h + 1;
+          if (c >= nsrv) break;
+          if (c + 1 < nsrv && heap[c + 1] < heap[c]) ++c;
+          if (!(heap[c] < f)) break;
+          heap[h] = heap[c];
+          h = c;
+        }
+        heap[h] = f;
+      }
+    }
+    __syncthreads();
+    for (uint32_t j = threadIdx.x; j < m; j += blockDim.x) {
+      start[base + j] = sA[j];
+      finish[base + j] = sB[j];
+    }
+  }
+  if (threadIdx.x == 0) {
+    *busy_out = busy;
+    *last_out = last;
+  }
+}
+
 __global__ void __launch_bounds__(256) request_kernel(QArgs Q) {
   __shared__ double s_sum[8];
   __shared__ unsigned long long s_min[8], s_max[8];
@@ -1625,73 +1689,85 @@ void trace_run(const TraceArgs& A, TraceResult* R, cudaStream_t s) {
                                                     A.bat_bin, A.bat_size);
     note_launch();
     BB_CK(cudaGetLastError());
-    // Lindley: certified busy-period splits, then exact serial segments
-    const uint32_t lt = nb ? (nb + LTILE - 1) / LTILE : 1;
-    double *aggA, *aggC, *incA, *incC, *busy_part, *busy_sum;
-    uint32_t* lflag;
-    BB_CK(pool.alloc((void**)&aggA, (size_t)lt * 8));
-    BB_CK(pool.alloc((void**)&aggC, (size_t)lt * 8));
-    BB_CK(pool.alloc((void**)&incA, (size_t)lt * 8));
-    BB_CK(pool.alloc((void**)&incC, (size_t)lt * 8));
-    BB_CK(pool.alloc((void**)&busy_part, (size_t)lt * 8));
+    double *busy_sum, *last_dev;
     BB_CK(pool.alloc((void**)&busy_sum, 8));
-    BB_CK(pool.alloc((void**)&lflag, (size_t)lt * 4));
-    BB_CK(cudaMemsetAsync(lflag, 0, (size_t)lt * 4, s));
-    const double tol_rel = (double)(nb + 4096) * 0x1.0p-50;
-    double* Dt;
-    BB_CK(pool.alloc((void**)&Dt, (size_t)nb * 8 + 8));
-    {
-      LArgs L{dR, dS, nb, split, Dt, busy_part, aggA, aggC, incA, incC, lflag, ws.counters + 1,
-              tol_rel};
-      if (nb) lindley_scan_kernel<<<lt, LB, 0, s>>>(L);
+    BB_CK(pool.alloc((void**)&last_dev, 8));
+    BB_CK(cudaMemsetAsync(last_dev, 0, 8, s));
+    if (A.n_servers > 1) {  // S servers: Kiefer-Wolfowitz, dispatch order
+      double* heap_g = nullptr;
+      if (A.n_servers > KW_HEAP) BB_CK(pool.alloc((void**)&heap_g, (size_t)A.n_servers * 8));
+      kw_dispatch_kernel<<<1, 256, 0, s>>>(dR, dS, nb, A.n_servers, heap_g, start, finish, busy_sum,
+                                           last_dev);
+      note_launch();
+      BB_CK(cudaGetLastError());
+    } else {
+      // Lindley: certified busy-period splits, then exact serial segments
+      const uint32_t lt = nb ? (nb + LTILE - 1) / LTILE : 1;
+      double *aggA, *aggC, *incA, *incC, *busy_part;
+      uint32_t* lflag;
+      BB_CK(pool.alloc((void**)&aggA, (size_t)lt * 8));
+      BB_CK(pool.alloc((void**)&aggC, (size_t)lt * 8));
+      BB_CK(pool.alloc((void**)&incA, (size_t)lt * 8));
+      BB_CK(pool.alloc((void**)&incC, (size_t)lt * 8));
+      BB_CK(pool.alloc((void**)&busy_part, (size_t)lt * 8));
+      BB_CK(pool.alloc((void**)&lflag, (size_t)lt * 4));
+      BB_CK(cudaMemsetAsync(lflag, 0, (size_t)lt * 4, s));
+      const double tol_rel = (double)(nb + 4096) * 0x1.0p-50;
+      double* Dt;
+      BB_CK(pool.alloc((void**)&Dt, (size_t)nb * 8 + 8));
+      {
+        LArgs L{dR, dS, nb, split, Dt, busy_part, aggA, aggC, incA, incC, lflag, ws.counters + 1,
+                tol_rel};
+        if (nb) lindley_scan_kernel<<<lt, LB, 0, s>>>(L);
+        note_launch();
+        BB_CK(cudaGetLastError());
+      }
+      // exact values: binade parity scan (parallel), serial segments only as a fallback
+      int* bad;
+      BB_CK(pool.alloc((void**)&bad, 4));
+      BB_CK(cudaMemsetAsync(bad, 0, 4, s));
+      if (nb) {
+        BArgs Bq{};
+        Bq.R = dR;
+        Bq.S = dS;
+        Bq.Dt = Dt;
+        Bq.code = split;
+        Bq.nb = nb;
+        Bq.tol_rel = tol_rel;
+        BB_CK(pool.alloc((void**)&Bq.p0, (size_t)nb * 8));
+        BB_CK(pool.alloc((void**)&Bq.p1, (size_t)nb * 8));
+        BB_CK(pool.alloc((void**)&Bq.head_of, (size_t)nb * 4));
+        BB_CK(pool.alloc((void**)&Bq.run_last, (size_t)nb * 4));
+        BB_CK(pool.alloc((void**)&Bq.ag0, (size_t)lt * 8));
+        BB_CK(pool.alloc((void**)&Bq.ag1, (size_t)lt * 8));
+        BB_CK(pool.alloc((void**)&Bq.in0, (size_t)lt * 8));
+        BB_CK(pool.alloc((void**)&Bq.in1, (size_t)lt * 8));
+        BB_CK(pool.alloc((void**)&Bq.agh, (size_t)lt * 4));
+        BB_CK(pool.alloc((void**)&Bq.inh, (size_t)lt * 4));
+        BB_CK(pool.alloc((void**)&Bq.agf, (size_t)lt * 4));
+        BB_CK(pool.alloc((void**)&Bq.inf, (size_t)lt * 4));
+        BB_CK(pool.alloc((void**)&Bq.flag, (size_t)lt * 4));
+        BB_CK(cudaMemsetAsync(Bq.flag, 0, (size_t)lt * 4, s));
+        Bq.counter = ws.counters + 2;
+        binade_scan_kernel<<<lt, LB, 0, s>>>(Bq);
+        note_launch();
+        BB_CK(cudaGetLastError());
+        binade_chain_kernel<<<grid_for(nb, 128), 128, 0, s>>>(dR, dS, Dt, split, Bq.p0, Bq.p1,
+                                                              Bq.run_last, nb, start, finish, bad);
+        note_launch();
+        BB_CK(cudaGetLastError());
+        binade_fill_kernel<<<grid_for(nb, 256), 256, 0, s>>>(dS, Dt, split, Bq.p0, Bq.p1, Bq.head_of,
+                                                             nb, tol_rel, start, finish, bad);
+        note_launch();
+        BB_CK(cudaGetLastError());
+        lindley_segments_kernel<<<grid_for(nb, 128), 128, 0, s>>>(dR, dS, split, nb, start, finish, bad);
+        note_launch();
+        BB_CK(cudaGetLastError());
+      }
+      sum_kernel<<<1, 256, 0, s>>>(busy_part, nb ? lt : 0, busy_sum);
       note_launch();
       BB_CK(cudaGetLastError());
     }
-    // exact values: binade parity scan (parallel), serial segments only as a fallback
-    int* bad;
-    BB_CK(pool.alloc((void**)&bad, 4));
-    BB_CK(cudaMemsetAsync(bad, 0, 4, s));
-    if (nb) {
-      BArgs Bq{};
-      Bq.R = dR;
-      Bq.S = dS;
-      Bq.Dt = Dt;
-      Bq.code = split;
-      Bq.nb = nb;
-      Bq.tol_rel = tol_rel;
-      BB_CK(pool.alloc((void**)&Bq.p0, (size_t)nb * 8));
-      BB_CK(pool.alloc((void**)&Bq.p1, (size_t)nb * 8));
-      BB_CK(pool.alloc((void**)&Bq.head_of, (size_t)nb * 4));
-      BB_CK(pool.alloc((void**)&Bq.run_last, (size_t)nb * 4));
-      BB_CK(pool.alloc((void**)&Bq.ag0, (size_t)lt * 8));
-      BB_CK(pool.alloc((void**)&Bq.ag1, (size_t)lt * 8));
-      BB_CK(pool.alloc((void**)&Bq.in0, (size_t)lt * 8));
-      BB_CK(pool.alloc((void**)&Bq.in1, (size_t)lt * 8));
-      BB_CK(pool.alloc((void**)&Bq.agh, (size_t)lt * 4));
-      BB_CK(pool.alloc((void**)&Bq.inh, (size_t)lt * 4));
-      BB_CK(pool.alloc((void**)&Bq.agf, (size_t)lt * 4));
-      BB_CK(pool.alloc((void**)&Bq.inf, (size_t)lt * 4));
-      BB_CK(pool.alloc((void**)&Bq.flag, (size_t)lt * 4));
-      BB_CK(cudaMemsetAsync(Bq.flag, 0, (size_t)lt * 4, s));
-      Bq.counter = ws.counters + 2;
-      binade_scan_kernel<<<lt, LB, 0, s>>>(Bq);
-      note_launch();
-      BB_CK(cudaGetLastError());
-      binade_chain_kernel<<<grid_for(nb, 128), 128, 0, s>>>(dR, dS, Dt, split, Bq.p0, Bq.p1,
-                                                            Bq.run_last, nb, start, finish, bad);
-      note_launch();
-      BB_CK(cudaGetLastError());
-      binade_fill_kernel<<<grid_for(nb, 256), 256, 0, s>>>(dS, Dt, split, Bq.p0, Bq.p1, Bq.head_of,
-                                                           nb, tol_rel, start, finish, bad);
-      note_launch();
-      BB_CK(cudaGetLastError());
-      lindley_segments_kernel<<<grid_for(nb, 128), 128, 0, s>>>(dR, dS, split, nb, start, finish, bad);
-      note_launch();
-      BB_CK(cudaGetLastError());
-    }
-    sum_kernel<<<1, 256, 0, s>>>(busy_part, nb ? lt : 0, busy_sum);
-    note_launch();
-    BB_CK(cudaGetLastError());
     // per-request pass
     unsigned long long *keys, *kminmax;
     double *lat_part, *lat_sum;
@@ -1734,7 +1810,8 @@ void trace_run(const TraceArgs& A, TraceResult* R, cudaStream_t s) {
     if (A.bat_first) BB_CK(cudaMemcpyAsync(A.bat_first, dfirst, (size_t)nb * 4, cudaMemcpyDeviceToDevice, s));
     double last = 0, a0 = 0, busy = 0, lsum = 0;
     unsigned long long mm[2];
-    if (nb) BB_CK(cudaMemcpyAsync(&last, finish + nb - 1, 8, cudaMemcpyDeviceToHost, s));
+    if (A.n_servers > 1) BB_CK(cudaMemcpyAsync(&last, last_dev, 8, cudaMemcpyDeviceToHost, s));
+    else if (nb) BB_CK(cudaMemcpyAsync(&last, finish + nb - 1, 8, cudaMemcpyDeviceToHost, s));
     BB_CK(cudaMemcpyAsync(&a0, A.a, 8, cudaMemcpyDeviceToHost, s));
     BB_CK(cudaMemcpyAsync(&busy, busy_sum, 8, cudaMemcpyDeviceToHost, s));
     BB_CK(cudaMemcpyAsync(&lsum, lat_sum, 8, cudaMemcpyDeviceToHost, s));
@@ -1745,7 +1822,7 @@ void trace_run(const TraceArgs& A, TraceResult* R, cudaStream_t s) {
       R->makespan = last - a0;
       R->throughput = (double)nc / R->makespan;
       R->busy = busy;
-      R->busy_fraction = busy / (1.0 * R->makespan);
+      R->busy_fraction = busy / ((double)(A.n_servers > 1 ? A.n_servers : 1) * R->makespan);
       R->latency_sum = lsum;
       R->latency_mean = lsum / (double)nc;
       // interpolated_quantile, binning.hpp:98-104

@@ -7,6 +7,7 @@ namespace bb {
 // Everything on the device; outputs optional (nullptr).
 struct TraceArgs {
   uint32_t n, B, k;
+  uint32_t n_servers;        // 0/1: Lindley scan; > 1: Kiefer-Wolfowitz dispatch
   int32_t flush;
   int32_t err_kind;          // 0 perfect, 1 symmetric, 2 confusion (needs u_err)
   double p_error;

@@ -1,8 +1,8 @@
 // The reference's simulator unit tests (proj/tests/test_simulator.cpp) and
 // acceptance criteria 1/2/7/8/10 (proj/tests/acceptance.cpp), rewritten
 // against the C++ drop-in header: the only change a reference user makes is
-// the include (binbatch_b200/binbatch.hpp) and the link line.  Multi-server
-// and max_batch_wait cases check that the GPU path reports them as not yet
+// the include (binbatch_b200/binbatch.hpp) and the link line.  The
+// max_batch_wait case checks that the GPU path reports it as not yet
 // implemented (std::logic_error) instead of silently falling back.
 #include <algorithm>
 #include <cmath>
@@ -239,11 +239,63 @@ int main() {
     cfg.bins = make_bin_config({1.0, 3.5, 6.0});
     CHECK(replay_trace(cfg, {1.0, 5.0, 2.0, 6.0}).makespan == 8.0);
   }
-  {  // multi-server / batch-wait: not yet on the GPU path -- reported, not faked
+  {  // all requests complete and appear in exactly one batch, 2 servers (:60-83)
     SimConfig cfg = overload_uniform(1003, 16, 3, 7);
+    cfg.arrival_rate = 5.0;
     cfg.n_servers = 2;
-    CHECK_THROWS(run_simulation(cfg), std::logic_error);
-    cfg = overload_uniform(400, 10, 4, 70);
+    cfg.flush_partial = true;
+    const SimResult result = run_simulation_detailed(cfg);
+    CHECK(result.metrics.n_completed == 1003);
+    std::set<std::size_t> seen;
+    std::size_t total = 0;
+    bool sizes_ok = true, complete_ok = true;
+    for (const BatchRecord& b : result.batches) {
+      total += b.members.size();
+      for (const std::size_t id : b.members) seen.insert(id);
+      sizes_ok &= b.members.size() <= 16;
+    }
+    for (const Request& r : result.requests)
+      complete_ok &= r.batch != kNoBatch && r.completion_time >= r.arrival_time;
+    CHECK(sizes_ok && complete_ok);
+    CHECK(total == 1003 && seen.size() == 1003);
+    std::size_t batch_sum = 0;
+    for (const std::size_t c : result.metrics.per_bin_batch_counts) batch_sum += c;
+    CHECK(batch_sum == result.batches.size());
+  }
+  {  // latency matches the closed form when servers are plentiful (:202-218)
+    SimConfig cfg;
+    cfg.arrival_rate = 2.0;
+    cfg.n_requests = 6400;
+    cfg.batch_size = 16;
+    cfg.bins = uniform_boundaries(2, 1.0, 20.0);
+    cfg.service = make_uniform(1.0, 20.0);
+    cfg.n_servers = 500;
+    double total = 0;
+    for (int rep = 0; rep < 5; ++rep) {
+      cfg.seed = 400 + rep;
+      total += run_simulation(cfg).latency_mean;
+    }
+    const double predicted = expected_latency(16, 2, 1.0, 20.0, 2.0);
+    CHECK(std::abs(total / 5 - predicted) / predicted < 0.05);
+  }
+  {  // equal-length traces remove all batching inefficiency, 2 servers (:277-291)
+    SimConfig cfg;
+    cfg.arrival_rate = kOverload;
+    cfg.n_requests = 64;
+    cfg.batch_size = 16;
+    cfg.bins = make_bin_config({0.5, 1.5});
+    cfg.n_servers = 2;
+    cfg.seed = 31;
+    cfg.trace_mode = TraceMode::cyclic;
+    const SimResult result = replay_trace_detailed(cfg, {1.0});
+    bool svc_ok = true;
+    for (const BatchRecord& b : result.batches) svc_ok &= b.service_time == 1.0;
+    CHECK(svc_ok);
+    CHECK(approx(result.metrics.makespan, 2.0, 1e-12));
+    CHECK(approx(result.metrics.throughput, 64.0 / 2.0, 1e-12));
+  }
+  {  // max_batch_wait: not yet on the GPU path -- reported, not faked
+    SimConfig cfg = overload_uniform(400, 10, 4, 70);
     cfg.max_batch_wait = 1.5;
     CHECK_THROWS(run_simulation(cfg), std::logic_error);
   }

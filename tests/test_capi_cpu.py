@@ -119,8 +119,6 @@ def test_replay_trace_validation():
 
 def test_outside_gpu_envelope_is_reported():
     with pytest.raises(NotImplementedError):
-        bb.run_simulation(cfg(n_servers=2))
-    with pytest.raises(NotImplementedError):
         bb.run_simulation(cfg(max_batch_wait=1.5))
 
 

@@ -219,3 +219,19 @@ def test_acceptance_criterion3_latency_formula():
         pred = bb.expected_latency(128, p.k, 1.0, 20.0, p.arrival_rate)
         assert abs(p.latency_mean - pred) / pred < 0.05
         assert p.analytic_latency == pytest.approx(pred)
+
+
+@pytest.mark.parametrize("S,k,flush", [(2, 3, True), (8, 4, False), (64, 2, True)])
+def test_multi_server_overload_vs_reference(S, k, flush):
+    # overload with S servers (paper Fig. 6: 8 servers): batches in dispatch
+    # order through the Kiefer-Wolfowitz recursion; 3-sigma vs the reference
+    B, n = 16, 2003
+    t = template(n_requests=n, batch_size=B, n_servers=S, flush_partial=flush,
+                 bins=bb.BinRule(k=k))
+    p = bb.run_point(t, 33, 2000)
+    thr, lat = ref_stats(dict(arrival_rate=math.inf, n_requests=n, batch_size=B, n_servers=S,
+                              flush_partial=flush,
+                              edges=bb.uniform_boundaries(k, 1.0, 20.0).edges, lo=1.0, hi=20.0),
+                         200)
+    assert within_3se(p.throughput_mean, p.throughput_std, 2000, thr)
+    assert within_3se(p.latency_mean, p.latency_std, 2000, lat)
