@@ -288,6 +288,10 @@ double bb_analytic_latency(uint64_t batch_size, uint64_t k, double lo, double hi
 /* Philox4x32-10 on the host (the same function the kernels inline), for
  * known-answer tests: out[4] = philox(ctr[4], key[2]). */
 void bb_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);
+/* The engine's exponential variates E = -log1p(-x 2^-53) (rng.hpp:43) of
+ * 53-bit keys, on the device: table = 1 the inter-arrival gap function,
+ * 0 the service-key function (accuracy tests). */
+bb_status bb_exponential_variates(const uint64_t* keys, uint64_t n, int32_t table, double* out);
 
 /* Kernel launches issued by this thread since the last reset (evidence for
  * bench.py's gpu_launches). */

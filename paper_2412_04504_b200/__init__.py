@@ -682,6 +682,18 @@ def philox4x32_10(ctr, key):
     return list(o)
 
 
+def exponential_variates(keys, table: bool = True):
+    """E = -log1p(-x 2^-53) for 53-bit keys x, computed on the device by the
+    engine's gap function (table=True) or its service-key function."""
+    import numpy as np
+    x = np.ascontiguousarray(keys, dtype=np.uint64)
+    out = np.empty(x.shape[0], dtype=np.float64)
+    _check(_lib.bb_exponential_variates(x.ctypes.data_as(C.POINTER(C.c_uint64)), x.shape[0],
+                                        int(bool(table)),
+                                        out.ctypes.data_as(C.POINTER(C.c_double))))
+    return out
+
+
 def launch_count(reset: bool = False) -> int:
     return int(_lib.bb_launch_count(int(reset)))
 

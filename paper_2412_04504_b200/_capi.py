@@ -112,6 +112,7 @@ EXPORTS = [
     "bb_uniform_boundaries", "bb_exponential_boundaries", "bb_empirical_boundaries",
     "bb_analytic_throughput", "bb_analytic_latency", "bb_philox4x32_10", "bb_launch_count",
     "bb_last_kernel_ms", "bb_points_shard_device", "bb_run_points", "bb_points_reduce_device", "bb_transfer_bytes",
+    "bb_exponential_variates",
 ]
 
 
@@ -158,6 +159,8 @@ def load():
     lib.bb_analytic_latency.restype = C.c_double
     lib.bb_analytic_latency.argtypes = [C.c_uint64, C.c_uint64, C.c_double, C.c_double, C.c_double]
     lib.bb_philox4x32_10.argtypes = [P(C.c_uint32), P(C.c_uint32), P(C.c_uint32)]
+    lib.bb_exponential_variates.restype = C.c_int
+    lib.bb_exponential_variates.argtypes = [P(C.c_uint64), C.c_uint64, C.c_int32, _dp]
     lib.bb_transfer_bytes.argtypes = [P(C.c_uint64), P(C.c_uint64), C.c_int]
     lib.bb_launch_count.restype = C.c_uint64
     lib.bb_launch_count.argtypes = [C.c_int]

@@ -19,24 +19,32 @@
 //     closed-form from a first counting pass; the second pass replays the
 //     same counter-based draws.
 #pragma once
+#include <type_traits>
+
 #include "bb_generated.cuh"
 
 namespace bb {
 namespace {
 
-constexpr int kGenThreads = 256;
+#ifndef BB_GEN_THREADS
+#define BB_GEN_THREADS 256
+#endif
+constexpr int kGenThreads = BB_GEN_THREADS;
 constexpr int kGenWarps = kGenThreads / 32;
 constexpr uint64_t kCntBits = 11;
 constexpr uint64_t kCntMask = (1ull << kCntBits) - 1;  // B <= 2047 in the packed state
 
 
 // 1 + #{j in 1..k-1 : thr[j] <= x}  (== assign_bin for monotone s(x))
-__device__ __forceinline__ uint32_t bin_of(const uint64_t* thr, const uint8_t* lut, bool lut_ok,
-                                           uint32_t k, uint32_t top, uint64_t x) {
-  if (lut_ok) {  // one table read + at most one threshold compare
-    const uint32_t c = lut[x >> 45];
-    return c + 1 + (c + 1 < k && thr[c + 1] <= x);
-  }
+// bucket path: one 8-byte table read and one compare, (x<<8 | 0xFF) >= bkt[b]
+// <=> x >= next (the low byte holds c <= 255)
+__device__ __forceinline__ uint32_t bin_bkt(const uint64_t* bkt, uint32_t shift, uint64_t x) {
+  const uint64_t e = bkt[x >> shift];
+  return (uint32_t)(e & 0xFF) + 1 + (((x << 8) | 0xFF) >= e);
+}
+__device__ __forceinline__ uint32_t bin_of(const uint64_t* thr, const uint64_t* bkt, bool bkt_ok,
+                                           uint32_t shift, uint32_t k, uint32_t top, uint64_t x) {
+  if (bkt_ok) return bin_bkt(bkt, shift, x);
   uint32_t pos = 0;
   for (uint32_t step = top; step; step >>= 1)
     if (pos + step < k && thr[pos + step] <= x) pos += step;
@@ -156,7 +164,10 @@ template <int SVC, int ERR, bool OVL, bool TRACK, bool MS>
 __global__ void __launch_bounds__(kGenThreads, BB_GEN_MINB) gen_kernel(const __grid_constant__ GenLaunch L) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ uint64_t s_thr[kGenWarps][BB_MAX_BINS + 1];
-  __shared__ __align__(16) uint8_t s_lut[kGenWarps][256];
+  __shared__ __align__(16) uint64_t s_bkt[kGenWarps][256];
+  __shared__ double2 s_logtab[kLogTab];
+  init_log_table(s_logtab);
+  __syncthreads();
   const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5, tid = threadIdx.x;
   const uint32_t kmax = L.k_max;
   uint64_t* st = reinterpret_cast<uint64_t*>(smem_raw);  // [kmax][T] packed (key<<11 | cnt)
@@ -178,7 +189,8 @@ __global__ void __launch_bounds__(kGenThreads, BB_GEN_MINB) gen_kernel(const __g
     const GenPoint& P = L.pts_dev[p];
     const uint32_t k = P.k, B = P.B, n = P.n;
     for (uint32_t j = lane; j <= k; j += 32) s_thr[wib][j] = P.thr[j];
-    reinterpret_cast<uint2*>(s_lut[wib])[lane] = reinterpret_cast<const uint2*>(P.lut)[lane];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) s_bkt[wib][lane + 32 * q] = P.bkt[lane + 32 * q];
     __syncwarp();
     const uint32_t r = L.rep_begin + c * 32 + lane;
     if (r < L.rep_end) {
@@ -190,8 +202,9 @@ __global__ void __launch_bounds__(kGenThreads, BB_GEN_MINB) gen_kernel(const __g
       const uint32_t* __restrict__ cyc_rank = P.cyc_rank;
       const uint64_t* __restrict__ conf_thr = P.conf_thr;
       const uint64_t* thr = s_thr[wib];
-      const uint8_t* lut = s_lut[wib];
-      const bool lut_ok = P.lut_ok != 0;
+      const uint64_t* bkt = s_bkt[wib];
+      const bool bkt_ok = P.bkt_ok != 0;
+      const uint32_t bshift = P.bkt_shift;
       const uint32_t top = k > 1 ? (1u << (31 - __clz(k - 1))) : 0u;
       const bool check = P.check_domain != 0;
       const uint64_t vlo = P.vlo, vhi = P.vhi, et1 = P.e_t1, et2 = P.e_t2;
@@ -203,8 +216,8 @@ __global__ void __launch_bounds__(kGenThreads, BB_GEN_MINB) gen_kernel(const __g
       double thr_out, lat_out, mk_out, busy_out;
 
       // bin of a key, then the error model (predict_bin, binning.hpp:231-261)
-      auto bin_pred = [&](uint64_t xs, uint64_t xe) -> uint32_t {
-        const uint32_t tb = k > 1 ? bin_of(thr, lut, lut_ok, k, top, xs) : 1u;
+      // the error model on a true bin (predict_bin, binning.hpp:231-261)
+      auto pred_of = [&](uint32_t tb, uint64_t xe) -> uint32_t {
         if (ERR == 1) {
           if (tb == 1) return xe < et1 ? 2u : 1u;
           if (tb == k) return xe < et1 ? k - 1 : k;
@@ -218,6 +231,9 @@ __global__ void __launch_bounds__(kGenThreads, BB_GEN_MINB) gen_kernel(const __g
           return pb;
         }
         return tb;
+      };
+      auto bin_pred = [&](uint64_t xs, uint64_t xe) -> uint32_t {
+        return pred_of(bin_of(thr, bkt, bkt_ok, bshift, k, top, xs), xe);
       };
       // the error stream's two uniforms for requests (2m, 2m+1)
       auto err_pair = [&](uint32_t i, uint64_t& e0, uint64_t& e1) {
@@ -243,7 +259,7 @@ __global__ void __launch_bounds__(kGenThreads, BB_GEN_MINB) gen_kernel(const __g
           for (uint32_t q = 0; q < srv.S; ++q) srv.V[(size_t)q * srv.stride] = 0.0;
         }
         uint32_t cyc0 = 0;
-        const double a0 = exp1_from_bits53_c(draw<SVC>(cyc_rank, nt, 0, c2, c3, cyc0).xg, L.coef) * inv_lambda;
+        const double a0 = exp1_tab(draw<SVC>(cyc_rank, nt, 0, c2, c3, cyc0).xg, s_logtab) * inv_lambda;
         // U requests per iteration: their draws, exponentials and bins are
         // independent, so the latencies overlap; the folds stay in order
         constexpr int U = BB_GEN_UNROLL;
@@ -264,60 +280,68 @@ __global__ void __launch_bounds__(kGenThreads, BB_GEN_MINB) gen_kernel(const __g
             err_pair(u, e[u], e[u + 1]);
           }
         }
-        for (; i + U <= n; i += U) {
-          double g[U];
-          uint32_t pb[U];
-          Draw dn[U];
-          uint64_t en[U];
-          if (!PIPE) {
+        // the bucket lookup is warp-uniform: one copy of the loop per path
+        auto main_loop = [&](auto bk) {
+          constexpr bool BK = decltype(bk)::value;
+          for (; i + U <= n; i += U) {
+            double g[U];
+            uint32_t pb[U];
+            Draw dn[U];
+            uint64_t en[U];
+            if (!PIPE) {
 #pragma unroll
-            for (int u = 0; u < U; ++u) d[u] = draw<SVC>(cyc_rank, nt, i + u, c2, c3, cyc);
+              for (int u = 0; u < U; ++u) d[u] = draw<SVC>(cyc_rank, nt, i + u, c2, c3, cyc);
 #pragma unroll
-            for (int u = 0; u < U; u += 2) {
-              e[u] = e[u + 1] = 0;
-              err_pair(i + u, e[u], e[u + 1]);
+              for (int u = 0; u < U; u += 2) {
+                e[u] = e[u + 1] = 0;
+                err_pair(i + u, e[u], e[u + 1]);
+              }
+            } else {
+#pragma unroll
+              for (int u = 0; u < U; ++u) dn[u] = draw<SVC>(cyc_rank, nt, i + U + u, c2, c3, cyc);
+#pragma unroll
+              for (int u = 0; u < U; u += 2) {
+                en[u] = en[u + 1] = 0;
+                err_pair(i + U + u, en[u], en[u + 1]);
+              }
             }
-          } else {
 #pragma unroll
-            for (int u = 0; u < U; ++u) dn[u] = draw<SVC>(cyc_rank, nt, i + U + u, c2, c3, cyc);
+            for (int u = 0; u < U; ++u) g[u] = exp1_tab(d[u].xg, s_logtab) * inv_lambda;
+            bool oos = false;
 #pragma unroll
-            for (int u = 0; u < U; u += 2) {
-              en[u] = en[u + 1] = 0;
-              err_pair(i + U + u, en[u], en[u + 1]);
+            for (int u = 0; u < U; ++u) oos |= out_of_support(d[u].xs);
+            if (oos) {  // first offending request (no dynamic indexing: keeps d[] in registers)
+              uint32_t bad = 0;
+              uint64_t bx = 0;
+#pragma unroll
+              for (int u = U - 1; u >= 0; --u)
+                if (out_of_support(d[u].xs)) bad = (uint32_t)u, bx = d[u].xs;
+              raise_error(L.err, i + bad, BB_EDOMAIN, svc_of_key_t<SVC>(svc, bx), r);
+              failed = true;
+              break;
             }
-          }
 #pragma unroll
-          for (int u = 0; u < U; ++u) g[u] = exp1_from_bits53_c(d[u].xg, L.coef) * inv_lambda;
-          bool oos = false;
-#pragma unroll
-          for (int u = 0; u < U; ++u) oos |= out_of_support(d[u].xs);
-          if (oos) {  // first offending request (no dynamic indexing: keeps d[] in registers)
-            uint32_t bad = 0;
-            uint64_t bx = 0;
-#pragma unroll
-            for (int u = U - 1; u >= 0; --u)
-              if (out_of_support(d[u].xs)) bad = (uint32_t)u, bx = d[u].xs;
-            raise_error(L.err, i + bad, BB_EDOMAIN, svc_of_key_t<SVC>(svc, bx), r);
-            failed = true;
-            break;
-          }
-#pragma unroll
-          for (int u = 0; u < U; ++u) pb[u] = bin_pred(d[u].xs, e[u]);
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            R.t += g[u];  // exponential inter-arrival, simulator.hpp:181
-            R.asum += R.t;
-            fold<SVC, TRACK, MS>(R, st + (pb[u] - 1) * kGenThreads + tid,
-                             s_osum + (pb[u] - 1) * kGenThreads + tid, d[u].xs, B, svc, srv);
-          }
-          if (PIPE) {
+            for (int u = 0; u < U; ++u)
+              pb[u] = pred_of(BK ? bin_bkt(bkt, bshift, d[u].xs)
+                                 : bin_of(thr, bkt, false, bshift, k, top, d[u].xs), e[u]);
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-              d[u] = dn[u];
-              e[u] = en[u];
+              R.t += g[u];  // exponential inter-arrival, simulator.hpp:181
+              R.asum += R.t;
+              fold<SVC, TRACK, MS>(R, st + (pb[u] - 1) * kGenThreads + tid,
+                               s_osum + (pb[u] - 1) * kGenThreads + tid, d[u].xs, B, svc, srv);
+            }
+            if (PIPE) {
+#pragma unroll
+              for (int u = 0; u < U; ++u) {
+                d[u] = dn[u];
+                e[u] = en[u];
+              }
             }
           }
-        }
+        };
+        if (bkt_ok) main_loop(std::true_type{});
+        else main_loop(std::false_type{});
         // tail: fewer than U requests left, one at a time
         for (; !failed && i < n; ++i) {
           const Draw d0 = draw<SVC>(cyc_rank, nt, i, c2, c3, cyc);
@@ -329,7 +353,7 @@ __global__ void __launch_bounds__(kGenThreads, BB_GEN_MINB) gen_kernel(const __g
             failed = true;
           } else {
             const uint32_t p0 = bin_pred(d0.xs, e0);
-            R.t += exp1_from_bits53_c(d0.xg, L.coef) * inv_lambda;
+            R.t += exp1_tab(d0.xg, s_logtab) * inv_lambda;
             R.asum += R.t;
             fold<SVC, TRACK, MS>(R, st + (p0 - 1) * kGenThreads + tid, s_osum + (p0 - 1) * kGenThreads + tid,
                       d0.xs, B, svc, srv);

@@ -31,25 +31,29 @@ __global__ void thresholds_kernel(GenPoint* pts, uint32_t n_points) {
     else s_above = lo;
   }
   __syncthreads();
-  // bucket lookup table over the top 8 key bits (53-bit keys only)
-  if (P.svc.key_domain == kKeyDomain53) {
+  // bucket table over the top 8 bits of the key domain
+  {
     __shared__ int s_multi;
+    uint32_t shift = 0;
+    while (shift < 56 && ((D - 1) >> shift) >= 256) ++shift;
     if (threadIdx.x == 0) s_multi = 0;
     __syncthreads();
     for (uint32_t b = threadIdx.x; b < 256; b += blockDim.x) {
-      const uint64_t lo = (uint64_t)b << 45, hi = lo + (1ull << 45);
+      const uint64_t lo = (uint64_t)b << shift, hi = lo + (1ull << shift);
       uint32_t c = 0, inside = 0;
       for (uint32_t j = 1; j < k; ++j) {
         c += P.thr[j] <= lo;
         inside += P.thr[j] > lo && P.thr[j] < hi;
       }
-      P.lut[b] = (uint8_t)c;
+      const uint64_t next = c + 1 < k ? P.thr[c + 1] : (1ull << 55);
+      P.bkt[b] = (next << 8) | c;
       if (inside > 1) atomicOr(&s_multi, 1);
     }
     __syncthreads();
-    if (threadIdx.x == 0) P.lut_ok = !s_multi;
-  } else if (threadIdx.x == 0) {
-    P.lut_ok = 0;
+    if (threadIdx.x == 0) {
+      P.bkt_shift = shift;
+      P.bkt_ok = !s_multi;
+    }
   }
   if (threadIdx.x == 0) {
     const uint64_t vlo = P.thr[0] > s_pos ? P.thr[0] : s_pos;

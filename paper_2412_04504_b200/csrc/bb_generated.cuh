@@ -21,10 +21,13 @@ struct GenPoint {
   const uint64_t* conf_thr; // confusion: k*k cumulative thresholds (device)
   const uint32_t* cyc_rank; // cyclic: sorted rank of lengths[j] (device)
   uint64_t thr[BB_MAX_BINS + 1];  // thr[j], j=1..k-1: bin > j <=> x >= thr[j]
-  // bin lookup: lut[x >> 45] = #{j : thr[j] <= bucket start}; valid when no
-  // 2^45-wide key bucket holds two thresholds (then one compare finishes)
-  uint8_t lut[256];
-  uint32_t lut_ok;
+  // bin lookup over 256 key buckets (x >> bkt_shift): bkt[b] = (next << 8) | c
+  // with c = #{j : thr[j] <= bucket start} and next = thr[c+1] (or 2^55 when
+  // c+1 == k); bin = c + 1 + (x >= next).  Exact when no bucket holds two
+  // thresholds (bkt_ok); otherwise the binary search over thr.
+  uint64_t bkt[256];
+  uint32_t bkt_shift;
+  uint32_t bkt_ok;
 };
 
 struct GenLaunch {

@@ -1353,6 +1353,21 @@ void bb_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out
   out[3] = r.w;
 }
 
+bb_status bb_exponential_variates(const uint64_t* keys, uint64_t n, int32_t table, double* out) {
+  return guarded([&] {
+    if (n && (!keys || !out)) raise(BB_EINVAL, "exponential variates: null buffer");
+    for (uint64_t i = 0; i < n; ++i)
+      if (keys[i] >= (1ull << 53)) raise(BB_EINVAL, "exponential variates: keys must be < 2^53");
+    const int dev = current_device(-1);
+    std::lock_guard<std::mutex> lock(g_ctx[dev].mu);
+    cudaStream_t st = ctx_stream(dev);
+    DBuf x = upload(keys, n, st), y(n * 8, st);
+    CK(bb::exp1_variates(x.as<uint64_t>(), n, table, y.as<double>(), st));
+    d2h(out, y.p, n * 8, st);
+    CK(cudaStreamSynchronize(st));
+  });
+}
+
 void bb_transfer_bytes(uint64_t* h2d_bytes, uint64_t* d2h_bytes, int reset) {
   if (h2d_bytes) *h2d_bytes = reset ? bb::g_h2d.exchange(0) : bb::g_h2d.load();
   if (d2h_bytes) *d2h_bytes = reset ? bb::g_d2h.exchange(0) : bb::g_d2h.load();

@@ -16,11 +16,16 @@ namespace {
 constexpr int MT = 256, MI = 8, MTILE = MT * MI;
 
 __global__ void draw_kernel(MatArgs M) {
+  __shared__ double2 s_logtab[kLogTab];
+  init_log_table(s_logtab);
+  __syncthreads();
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= M.n) return;
   const uint4 r = philox(i, kStreamArrivalService, M.c2, M.c3);
   const uint64_t xg = bits53(r.x, r.y);
-  M.gap[i] = M.overload ? 0.0 : exp1_from_bits53(xg) * M.inv_lambda;
+  // the fused kernel's gap variate (bb_gen_kernel.cuh), so a materialized
+  // replica equals the fused one
+  M.gap[i] = M.overload ? 0.0 : exp1_tab(xg, s_logtab) * M.inv_lambda;
   uint64_t xs;
   if (M.svc.kind == kSvcCyclic) xs = M.cyc_rank[i % M.svc.n_table];
   else xs = bits53(r.z, r.w);
@@ -139,6 +144,24 @@ cudaError_t materialize_streams(const MatArgs& M, double* arrivals, cudaStream_t
   cudaFreeAsync(incv, s);
   cudaFreeAsync(flag, s);
   return e;
+}
+
+__global__ void exp1_kernel(const uint64_t* __restrict__ x, uint64_t n, int table,
+                            double* __restrict__ out) {
+  __shared__ double2 s_logtab[kLogTab];
+  init_log_table(s_logtab);
+  __syncthreads();
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = table ? exp1_tab(x[i], s_logtab) : exp1_from_bits53(x[i]);
+}
+
+cudaError_t exp1_variates(const uint64_t* x, uint64_t n, int table, double* out, cudaStream_t s) {
+  if (!n) return cudaSuccess;
+  const uint64_t blocks = (n + 255) / 256;
+  exp1_kernel<<<(unsigned)(blocks < 4096 ? blocks : 4096), 256, 0, s>>>(x, n, table, out);
+  note_launch();
+  return cudaGetLastError();
 }
 
 }  // namespace bb

@@ -19,5 +19,8 @@ struct MatArgs {
 
 // Draws gaps/services/error uniforms and scans gaps into `arrivals`.
 cudaError_t materialize_streams(const MatArgs& M, double* arrivals, cudaStream_t s);
+// E = -log1p(-x 2^-53) for 53-bit keys: table = 1 the gap variate of the
+// generated engine (exp1_tab), 0 the service-key variate (exp1_from_bits53).
+cudaError_t exp1_variates(const uint64_t* x, uint64_t n, int table, double* out, cudaStream_t s);
 
 }  // namespace bb
