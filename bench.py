@@ -218,6 +218,8 @@ def main():
     ap.add_argument("--ref-reps", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-trace", action="store_true")
+    ap.add_argument("--no-quantiles", action="store_true",
+                    help="A/B only: skip the per-replication p50/p99 the reference computes")
     ap.add_argument("--dist-backend", default="nccl", help="nccl (default) or gloo for testing")
     args = ap.parse_args()
     if args.impl == "reference":
@@ -228,6 +230,8 @@ def main():
 
     import paper_2412_04504_b200 as bb
 
+    if args.no_quantiles:
+        bb.set_generated_quantiles(False)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))

@@ -293,6 +293,11 @@ void bb_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out
  * 0 the service-key function (accuracy tests). */
 bb_status bb_exponential_variates(const uint64_t* keys, uint64_t n, int32_t table, double* out);
 
+/* Generated mode computes every replication's exact latency p50/p99 like the
+ * reference's finish() (simulator.hpp:289-301), on by default.  Turning it off
+ * (A/B measurements only) leaves p50/p99 NaN.  Returns the previous setting. */
+int bb_set_generated_quantiles(int on);
+
 /* Kernel launches issued by this thread since the last reset (evidence for
  * bench.py's gpu_launches). */
 uint64_t bb_launch_count(int reset);

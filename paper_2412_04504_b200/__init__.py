@@ -694,6 +694,13 @@ def exponential_variates(keys, table: bool = True):
     return out
 
 
+def set_generated_quantiles(on: bool) -> bool:
+    """Exact per-replication p50/p99 in generated mode (default on, like the
+    reference's finish()); off leaves them NaN (A/B measurement only).
+    Returns the previous setting."""
+    return bool(_lib.bb_set_generated_quantiles(int(bool(on))))
+
+
 def launch_count(reset: bool = False) -> int:
     return int(_lib.bb_launch_count(int(reset)))
 

@@ -112,7 +112,7 @@ EXPORTS = [
     "bb_uniform_boundaries", "bb_exponential_boundaries", "bb_empirical_boundaries",
     "bb_analytic_throughput", "bb_analytic_latency", "bb_philox4x32_10", "bb_launch_count",
     "bb_last_kernel_ms", "bb_points_shard_device", "bb_run_points", "bb_points_reduce_device", "bb_transfer_bytes",
-    "bb_exponential_variates",
+    "bb_exponential_variates", "bb_set_generated_quantiles",
 ]
 
 
@@ -166,4 +166,6 @@ def load():
     lib.bb_launch_count.argtypes = [C.c_int]
     lib.bb_last_kernel_ms.restype = C.c_double
     lib.bb_last_kernel_ms.argtypes = [P(C.c_char_p)]
+    lib.bb_set_generated_quantiles.restype = C.c_int
+    lib.bb_set_generated_quantiles.argtypes = [C.c_int]
     return lib

@@ -22,6 +22,7 @@
 #include <type_traits>
 
 #include "bb_generated.cuh"
+#include "bb_quantile.cuh"
 
 namespace bb {
 namespace {
@@ -109,7 +110,7 @@ struct Servers {
 // MS selects the S-server code at compile time so that the one-server kernel
 // keeps its register budget (128 regs, 16 warps/SM).
 template <bool MS>
-__device__ __forceinline__ void dispatch(Rep& R, const Servers& sv, double S, uint32_t members) {
+__device__ __forceinline__ double dispatch(Rep& R, const Servers& sv, double S, uint32_t members) {
   double fin;
   if (!MS) {
     fin = R.D = __dadd_rn(fmax(R.D, R.t), S);
@@ -130,27 +131,50 @@ __device__ __forceinline__ void dispatch(Rep& R, const Servers& sv, double S, ui
   R.busy += S;
   R.latw += (double)members * fin;
   R.ncomp += members;
+  return fin;
 }
 
+// Quantile mode (bb_quantile.cuh): the forward pass's request log, this
+// lane's view of its warp's interleaved rows (layout in bb_quantile.cuh).
+struct QLog {
+  double* A;       // arrival of request i at A[(i/32)*1024 + i%32]
+  uint8_t* Bf;     // (bin - 1) | closed << 7 at Bf[(i/32)*1024 + i%32]
+  double* F;       // completion of full batch c (closing order) at F[c*32]
+  double* P;       // per bin: the drained partial's completion (NaN: none) at P[b*32]
+  uint32_t nc;     // full batches closed
+  double lmin, lmax;
+};
+
 // One request folded into its bin; closes the batch at B members
-// (on_arrival + form_batch, simulator.hpp:187-254).
-template <int SVC, bool track, bool MS>
-__device__ __forceinline__ void fold(Rep& R, uint64_t* __restrict__ slot, double* __restrict__ osum,
-                                     uint64_t xs, uint32_t B, const SvcParams& svc,
-                                     const Servers& sv) {
+// (on_arrival + form_batch, simulator.hpp:187-254).  Returns 1 when it closed.
+template <int SVC, bool track, bool MS, bool Q>
+__device__ __forceinline__ uint32_t fold(Rep& R, uint64_t* __restrict__ slot, double* __restrict__ osum,
+                                         uint64_t xs, uint32_t B, const SvcParams& svc,
+                                         const Servers& sv, QLog& q, uint32_t b) {
   const uint64_t s0 = *slot;
   const uint64_t km = max(s0 & ~kCntMask, xs << kCntBits);
   const uint32_t cnt = (uint32_t)(s0 & kCntMask) + 1;
   if (cnt == B) {
     *slot = 0;
-    dispatch<MS>(R, sv, svc_of_key_t<SVC>(svc, km >> kCntBits), B);
+    const double fin = dispatch<MS>(R, sv, svc_of_key_t<SVC>(svc, km >> kCntBits), B);
     if (track) *osum = 0.0;
-  } else {
-    *slot = km | cnt;
-    if (track) *osum += R.t;
+    if (Q) {  // osum is the bin's previous closing time in quantile mode
+      q.F[(size_t)(q.nc++) * 32] = fin;
+      const double lo = __dsub_rn(fin, R.t), hi = __dsub_rn(fin, *osum);
+      q.lmin = lo < q.lmin ? lo : q.lmin;  // closing member: the batch's smallest latency
+      q.lmax = hi > q.lmax ? hi : q.lmax;  // bounds the first member's (it arrived later)
+      *osum = R.t;
+    }
+    return 1u;
   }
+  *slot = km | cnt;
+  if (track) *osum += R.t;
+  return 0u;
 }
 
+#ifndef BB_QSTAGE
+#define BB_QSTAGE 3  // A/B only: 1 = request log, 2 = + latencies, 3 = + selection
+#endif
 #ifndef BB_GEN_MINB
 #define BB_GEN_MINB 1
 #endif
@@ -160,8 +184,19 @@ __device__ __forceinline__ void fold(Rep& R, uint64_t* __restrict__ slot, double
 #ifndef BB_GEN_UNROLL
 #define BB_GEN_UNROLL 4  // requests in flight per thread (even)
 #endif
-template <int SVC, int ERR, bool OVL, bool TRACK, bool MS>
-__global__ void __launch_bounds__(kGenThreads, BB_GEN_MINB) gen_kernel(const __grid_constant__ GenLaunch L) {
+// shared bytes of one warp's state rows, and of its whole region
+// (quantile mode, finite rate: the second row set holds each bin's previous
+// closing time instead of the open arrival sums)
+__host__ __device__ __forceinline__ uint32_t gen_state_bytes(uint32_t kmax, bool ovl, bool track, bool q) {
+  return kmax * 256u * (ovl ? 3u : ((track || q) ? 2u : 1u));
+}
+__host__ __device__ __forceinline__ uint32_t gen_warp_bytes(uint32_t kmax, bool ovl, bool track, bool q) {
+  const uint32_t st = gen_state_bytes(kmax, ovl, track, q);
+  return q ? (st > kQRegionMin ? st : kQRegionMin) + kmax * 8u + 32u : st;
+}
+
+template <int SVC, int ERR, bool OVL, bool TRACK, bool MS, bool Q>
+__global__ void __launch_bounds__(kGenThreads, Q ? 2 : BB_GEN_MINB) gen_kernel(const __grid_constant__ GenLaunch L) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ uint64_t s_thr[kGenWarps][BB_MAX_BINS + 1];
   __shared__ __align__(16) uint64_t s_bkt[kGenWarps][256];
@@ -170,12 +205,21 @@ __global__ void __launch_bounds__(kGenThreads, BB_GEN_MINB) gen_kernel(const __g
   __syncthreads();
   const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5, tid = threadIdx.x;
   const uint32_t kmax = L.k_max;
-  uint64_t* st = reinterpret_cast<uint64_t*>(smem_raw);  // [kmax][T] packed (key<<11 | cnt)
-  double* s_osum = reinterpret_cast<double*>(st + (size_t)kmax * kGenThreads);  // finite, no flush
-  uint32_t* s_F = reinterpret_cast<uint32_t*>(st + (size_t)kmax * kGenThreads);  // overload
-  uint32_t* s_rem = s_F + (size_t)kmax * kGenThreads;
-  uint32_t* s_cf = s_rem + (size_t)kmax * kGenThreads;
-  uint32_t* s_jd = s_cf + (size_t)kmax * kGenThreads;
+  // per-warp shared region: state rows of 32 lanes ([kmax] packed (key<<11 | cnt),
+  // then open arrival sums (finite, no flush) or four u32 tables (overload));
+  // in quantile mode the same region then holds the selection histogram
+  const uint32_t wbytes = gen_warp_bytes(kmax, OVL, TRACK, Q);
+  unsigned char* wreg = smem_raw + (size_t)wib * wbytes;
+  uint64_t* st = reinterpret_cast<uint64_t*>(wreg);
+  double* s_osum = reinterpret_cast<double*>(st + (size_t)kmax * 32);  // finite, no flush
+  uint32_t* s_F = reinterpret_cast<uint32_t*>(st + (size_t)kmax * 32);  // overload
+  uint32_t* s_rem = s_F + (size_t)kmax * 32;
+  uint32_t* s_cf = s_rem + (size_t)kmax * 32;
+  uint32_t* s_jd = s_cf + (size_t)kmax * 32;
+  const uint32_t qregion = gen_state_bytes(kmax, OVL, TRACK, Q) > kQRegionMin
+                               ? gen_state_bytes(kmax, OVL, TRACK, Q) : kQRegionMin;
+  double* q_carry = reinterpret_cast<double*>(wreg + qregion);  // [kmax]
+  double* q_ans = q_carry + kmax;                                  // [4]
 
   const uint32_t nrep = L.rep_end - L.rep_begin;
   const uint32_t chunks = (nrep + 31) / 32;
@@ -193,6 +237,16 @@ __global__ void __launch_bounds__(kGenThreads, BB_GEN_MINB) gen_kernel(const __g
     for (int q = 0; q < 8; ++q) s_bkt[wib][lane + 32 * q] = P.bkt[lane + 32 * q];
     __syncwarp();
     const uint32_t r = L.rep_begin + c * 32 + lane;
+    // quantile mode: this lane's request log and what the warp's selection needs
+    const size_t qslot = (size_t)blockIdx.x * kGenThreads + tid;
+    const size_t qwarp = (size_t)blockIdx.x * kGenWarps + wib;
+    QLog q{nullptr, nullptr, nullptr, nullptr, 0u, CUDART_INF, 0.0};
+    bool q_ok = false;
+    uint64_t q_m = 0;
+    uint32_t q_nb = 0;
+    double q_p50 = BB_QNAN, q_p99 = BB_QNAN;
+    double thr_out = 0.0, lat_out = 0.0, mk_out = 0.0, busy_out = 0.0;
+    const size_t gstride = (size_t)gridDim.x * blockDim.x;
     if (r < L.rep_end) {
       const uint64_t seed = L.single_seed ? L.master : replication_seed(L.master, r);
       const uint64_t sw = splitmix64(seed);  // RandomStream(seed) whitening, rng.hpp:30
@@ -210,10 +264,9 @@ __global__ void __launch_bounds__(kGenThreads, BB_GEN_MINB) gen_kernel(const __g
       const uint64_t vlo = P.vlo, vhi = P.vhi, et1 = P.e_t1, et2 = P.e_t2;
       const bool flush = P.flush != 0;
       const uint32_t nt = svc.n_table;
-      for (uint32_t b = 0; b < k; ++b) st[b * kGenThreads + tid] = 0;
+      for (uint32_t b = 0; b < k; ++b) st[b * 32 + lane] = 0;
       uint32_t cyc = 0;
       bool failed = false;
-      double thr_out, lat_out, mk_out, busy_out;
 
       // bin of a key, then the error model (predict_bin, binning.hpp:231-261)
       // the error model on a true bin (predict_bin, binning.hpp:231-261)
@@ -249,9 +302,16 @@ __global__ void __launch_bounds__(kGenThreads, BB_GEN_MINB) gen_kernel(const __g
         // ------------------------------------------------ finite arrival rate
         const double inv_lambda = P.inv_lambda;
         constexpr bool track = TRACK;  // no flush at a finite rate: leftover sums needed
-        if (track)
-          for (uint32_t b = 0; b < k; ++b) s_osum[b * kGenThreads + tid] = 0.0;
+        static_assert(!(TRACK && Q), "quantile mode sums the latencies themselves");
+        if (track || Q)  // (Q: previous closing time per bin)
+          for (uint32_t b = 0; b < k; ++b) s_osum[b * 32 + lane] = 0.0;
         Rep R{0.0, 0.0, 0.0, 0.0, 0.0, 0};
+        if (Q) {
+          q.A = L.qA + qwarp * L.q_n * 32 + lane * 32;
+          q.Bf = L.qB + qwarp * L.q_n * 32 + lane * 32;
+          q.F = L.qF + qwarp * L.q_nf * 32 + lane;
+          q.P = L.qP + qwarp * kmax * 32 + lane;
+        }
         Servers srv{MS && P.n_servers ? P.n_servers : 1u, nullptr, 0};
         if (MS && srv.S > 1) {  // all servers idle at t = 0
           srv.stride = gridDim.x * blockDim.x;
@@ -259,10 +319,11 @@ __global__ void __launch_bounds__(kGenThreads, BB_GEN_MINB) gen_kernel(const __g
           for (uint32_t q = 0; q < srv.S; ++q) srv.V[(size_t)q * srv.stride] = 0.0;
         }
         uint32_t cyc0 = 0;
-        const double a0 = exp1_tab(draw<SVC>(cyc_rank, nt, 0, c2, c3, cyc0).xg, s_logtab) * inv_lambda;
+        const double a0 = __dmul_rn(exp1_tab(draw<SVC>(cyc_rank, nt, 0, c2, c3, cyc0).xg, s_logtab), inv_lambda);
         // U requests per iteration: their draws, exponentials and bins are
         // independent, so the latencies overlap; the folds stay in order
         constexpr int U = BB_GEN_UNROLL;
+        static_assert(!Q || U % 4 == 0, "the request log packs 4 requests per lane");
         // software pipeline: the next group's Philox blocks (integer pipes)
         // are issued in the same basic block as this group's exponentials
         // (fp64 pipe) so the scheduler interleaves them (cyclic traces keep a
@@ -306,7 +367,7 @@ __global__ void __launch_bounds__(kGenThreads, BB_GEN_MINB) gen_kernel(const __g
               }
             }
 #pragma unroll
-            for (int u = 0; u < U; ++u) g[u] = exp1_tab(d[u].xg, s_logtab) * inv_lambda;
+            for (int u = 0; u < U; ++u) g[u] = __dmul_rn(exp1_tab(d[u].xg, s_logtab), inv_lambda);
             bool oos = false;
 #pragma unroll
             for (int u = 0; u < U; ++u) oos |= out_of_support(d[u].xs);
@@ -324,12 +385,29 @@ __global__ void __launch_bounds__(kGenThreads, BB_GEN_MINB) gen_kernel(const __g
             for (int u = 0; u < U; ++u)
               pb[u] = pred_of(BK ? bin_bkt(bkt, bshift, d[u].xs)
                                  : bin_of(thr, bkt, false, bshift, k, top, d[u].xs), e[u]);
+            uint32_t cl[U];
+            double at[U];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-              R.t += g[u];  // exponential inter-arrival, simulator.hpp:181
+              R.t = __dadd_rn(R.t, g[u]);  // exponential inter-arrival, simulator.hpp:181 (no contraction)
               R.asum += R.t;
-              fold<SVC, TRACK, MS>(R, st + (pb[u] - 1) * kGenThreads + tid,
-                               s_osum + (pb[u] - 1) * kGenThreads + tid, d[u].xs, B, svc, srv);
+              at[u] = R.t;
+              cl[u] = fold<SVC, TRACK, MS, Q>(R, st + (pb[u] - 1) * 32 + lane,
+                                              s_osum + (pb[u] - 1) * 32 + lane, d[u].xs, B, svc,
+                                              srv, q, pb[u] - 1);
+            }
+            if (Q) {  // request log: arrivals (16 B stores) and (bin | closed) bytes
+#pragma unroll
+              for (int u = 0; u < U; u += 2)
+                *reinterpret_cast<double2*>(q.A + (size_t)((i + u) >> 5) * 1024 + ((i + u) & 31)) =
+                    make_double2(at[u], at[u + 1]);
+#pragma unroll
+              for (int u = 0; u < U; u += 4) {
+                uint32_t w4 = 0;
+#pragma unroll
+                for (int v = 0; v < 4 && u + v < U; ++v) w4 |= ((pb[u + v] - 1) | (cl[u + v] << 7)) << (8 * v);
+                *reinterpret_cast<uint32_t*>(q.Bf + (size_t)((i + u) >> 5) * 1024 + ((i + u) & 31)) = w4;
+              }
             }
             if (PIPE) {
 #pragma unroll
@@ -353,22 +431,37 @@ __global__ void __launch_bounds__(kGenThreads, BB_GEN_MINB) gen_kernel(const __g
             failed = true;
           } else {
             const uint32_t p0 = bin_pred(d0.xs, e0);
-            R.t += exp1_tab(d0.xg, s_logtab) * inv_lambda;
+            R.t = __dadd_rn(R.t, __dmul_rn(exp1_tab(d0.xg, s_logtab), inv_lambda));
             R.asum += R.t;
-            fold<SVC, TRACK, MS>(R, st + (p0 - 1) * kGenThreads + tid, s_osum + (p0 - 1) * kGenThreads + tid,
-                      d0.xs, B, svc, srv);
+            const uint32_t c0 = fold<SVC, TRACK, MS, Q>(R, st + (p0 - 1) * 32 + lane,
+                                                        s_osum + (p0 - 1) * 32 + lane, d0.xs, B,
+                                                        svc, srv, q, p0 - 1);
+            if (Q) {
+              q.A[(size_t)(i >> 5) * 1024 + (i & 31)] = R.t;
+              q.Bf[(size_t)(i >> 5) * 1024 + (i & 31)] = (uint8_t)((p0 - 1) | (c0 << 7));
+            }
           }
         }
         double leftover = 0.0;
         if (!failed) {
           for (uint32_t b = 0; b < k; ++b) {
-            const uint64_t s0 = st[b * kGenThreads + tid];
+            const uint64_t s0 = st[b * 32 + lane];
             const uint32_t cnt = (uint32_t)(s0 & kCntMask);
-            if (!cnt) continue;
+            if (!cnt) {
+              if (Q) q.P[b * 32] = BB_QNAN;
+              continue;
+            }
             if (flush) {  // on_drain partials at the last arrival, bin order
-              dispatch<MS>(R, srv, svc_of_key_t<SVC>(svc, s0 >> kCntBits), cnt);
+              const double fin = dispatch<MS>(R, srv, svc_of_key_t<SVC>(svc, s0 >> kCntBits), cnt);
+              if (Q) {
+                q.P[b * 32] = fin;
+                const double lo = __dsub_rn(fin, R.t), hi = __dsub_rn(fin, s_osum[b * 32 + lane]);
+                q.lmin = lo < q.lmin ? lo : q.lmin;
+                q.lmax = hi > q.lmax ? hi : q.lmax;
+              }
             } else {
-              leftover += s_osum[b * kGenThreads + tid];
+              leftover += s_osum[b * 32 + lane];
+              if (Q) q.P[b * 32] = BB_QNAN;  // never completes
             }
           }
         }
@@ -377,14 +470,16 @@ __global__ void __launch_bounds__(kGenThreads, BB_GEN_MINB) gen_kernel(const __g
           thr_out = (double)R.ncomp / mk_out;
           busy_out = R.busy / ((double)srv.S * mk_out);  // simulator.hpp:287-288
           lat_out = (R.latw - (R.asum - leftover)) / (double)R.ncomp;
+          q_ok = Q;
+          q_m = R.ncomp;
         } else {
           mk_out = thr_out = busy_out = lat_out = failed ? BB_QNAN : 0.0;
         }
       } else {
         // ------------------------------------------------------- overload
         for (uint32_t b = 0; b < k; ++b) {
-          s_F[b * kGenThreads + tid] = 0;
-          s_cf[b * kGenThreads + tid] = 0xFFFFFFFFu;
+          s_F[b * 32 + lane] = 0;
+          s_cf[b * 32 + lane] = 0xFFFFFFFFu;
         }
         uint64_t e0 = 0, e1 = 0;
         for (uint32_t i = 0; i < n; ++i) {  // pass 1: per-bin totals, first closings
@@ -396,18 +491,18 @@ __global__ void __launch_bounds__(kGenThreads, BB_GEN_MINB) gen_kernel(const __g
             break;
           }
           const uint32_t pb = bin_pred(d.xs, (i & 1u) ? e1 : e0);
-          const uint32_t cnt = ++s_F[(pb - 1) * kGenThreads + tid];
-          if (cnt == B) s_cf[(pb - 1) * kGenThreads + tid] = i;
+          const uint32_t cnt = ++s_F[(pb - 1) * 32 + lane];
+          if (cnt == B) s_cf[(pb - 1) * 32 + lane] = i;
         }
         if (!failed) {
           uint32_t Z = 0;
           uint64_t nc = 0;
           for (uint32_t b = 0; b < k; ++b) {
-            const uint32_t cnt = s_F[b * kGenThreads + tid];
+            const uint32_t cnt = s_F[b * 32 + lane];
             const uint32_t F = cnt / B, rem = cnt - F * B;
-            s_F[b * kGenThreads + tid] = F;
-            s_rem[b * kGenThreads + tid] = rem;
-            s_jd[b * kGenThreads + tid] = 0;
+            s_F[b * 32 + lane] = F;
+            s_rem[b * 32 + lane] = rem;
+            s_jd[b * 32 + lane] = 0;
             Z += F >= 1;
             nc += (uint64_t)F * B + (flush ? rem : 0);
           }
@@ -415,38 +510,37 @@ __global__ void __launch_bounds__(kGenThreads, BB_GEN_MINB) gen_kernel(const __g
           double busy = 0.0, latw = 0.0;
           // S > 1 servers: pass 2 files each batch (service, members) under its
           // dispatch index, then the Kiefer-Wolfowitz recursion runs in order
-          const size_t gstride = (size_t)gridDim.x * blockDim.x;
-          double* ovS = MS ? L.ovS + (size_t)blockIdx.x * blockDim.x + tid : nullptr;
-          uint16_t* ovM = MS ? L.ovM + (size_t)blockIdx.x * blockDim.x + tid : nullptr;
+          double* ovS = (MS || Q) ? L.ovS + qslot : nullptr;
+          uint16_t* ovM = (MS || Q) ? L.ovM + qslot : nullptr;
           for (uint32_t i = 0; i < n; ++i) {  // pass 2: same draws, batch positions
             const Draw d = draw<SVC>(cyc_rank, nt, i, c2, c3, cyc);
             if ((i & 1u) == 0) err_pair(i, e0, e1);
             const uint32_t pb = bin_pred(d.xs, (i & 1u) ? e1 : e0);
-            uint64_t* slot = st + (pb - 1) * kGenThreads + tid;
+            uint64_t* slot = st + (pb - 1) * 32 + lane;
             const uint64_t s0 = *slot;
             const uint64_t km = max(s0 & ~kCntMask, d.xs << kCntBits);
             const uint32_t cnt = (uint32_t)(s0 & kCntMask) + 1;
             if (cnt == B) {
               *slot = 0;
               const uint32_t b = pb - 1;
-              const uint32_t j = s_jd[b * kGenThreads + tid]++;
-              const uint32_t cfb = s_cf[b * kGenThreads + tid];
+              const uint32_t j = s_jd[b * 32 + lane]++;
+              const uint32_t cfb = s_cf[b * 32 + lane];
               uint64_t before;  // requests dispatched before this batch
               uint32_t idx;     // batches dispatched before this batch
               if (flush && j > 0) {  // drain phase, bins in order (on_drain, :218-221)
                 before = (uint64_t)B * Z + (uint64_t)B * (j - 1);
                 idx = Z + (j - 1);
                 for (uint32_t q = 0; q < b; ++q) {
-                  const uint32_t F = s_F[q * kGenThreads + tid];
-                  const uint32_t rq = s_rem[q * kGenThreads + tid];
+                  const uint32_t F = s_F[q * 32 + lane];
+                  const uint32_t rq = s_rem[q * 32 + lane];
                   before += (uint64_t)B * (F ? F - 1 : 0) + rq;
                   idx += (F ? F - 1 : 0) + (rq != 0);
                 }
               } else {  // round j, first-closing order (on_formation, :208-216)
                 uint64_t pos = 0;
                 for (uint32_t q = 0; q < k; ++q) {
-                  const uint32_t F = s_F[q * kGenThreads + tid];
-                  const uint32_t cq = s_cf[q * kGenThreads + tid];
+                  const uint32_t F = s_F[q * 32 + lane];
+                  const uint32_t cq = s_cf[q * 32 + lane];
                   if (!flush) pos += F < j ? F : j;
                   pos += (cq < cfb) && (F > j);
                 }
@@ -454,10 +548,11 @@ __global__ void __launch_bounds__(kGenThreads, BB_GEN_MINB) gen_kernel(const __g
                 idx = (uint32_t)pos;
               }
               const double S = svc_of_key_t<SVC>(svc, km >> kCntBits);
-              if (MS) {
+              if (MS || Q) {
                 ovS[idx * gstride] = S;
                 ovM[idx * gstride] = (uint16_t)B;
-              } else {
+              }
+              if (!MS) {
                 busy += S;
                 latw += S * (double)(nc - before);
               }
@@ -466,21 +561,22 @@ __global__ void __launch_bounds__(kGenThreads, BB_GEN_MINB) gen_kernel(const __g
             }
           }
           uint32_t nbt = 0;  // batches in total
-          for (uint32_t b = 0; b < k; ++b) nbt += s_F[b * kGenThreads + tid];
+          for (uint32_t b = 0; b < k; ++b) nbt += s_F[b * 32 + lane];
           if (flush) {
             uint64_t base = (uint64_t)B * Z;
             nbt = Z;
             for (uint32_t b = 0; b < k; ++b) {
-              const uint32_t F = s_F[b * kGenThreads + tid];
-              const uint32_t rem = s_rem[b * kGenThreads + tid];
+              const uint32_t F = s_F[b * 32 + lane];
+              const uint32_t rem = s_rem[b * 32 + lane];
               base += (uint64_t)B * (F ? F - 1 : 0);
               nbt += F ? F - 1 : 0;
               if (rem) {
-                const double S = svc_of_key_t<SVC>(svc, st[b * kGenThreads + tid] >> kCntBits);
-                if (MS) {
+                const double S = svc_of_key_t<SVC>(svc, st[b * 32 + lane] >> kCntBits);
+                if (MS || Q) {
                   ovS[(size_t)nbt * gstride] = S;
                   ovM[(size_t)nbt * gstride] = (uint16_t)rem;
-                } else {
+                }
+                if (!MS) {
                   busy += S;
                   latw += S * (double)(nc - base);
                 }
@@ -495,17 +591,34 @@ __global__ void __launch_bounds__(kGenThreads, BB_GEN_MINB) gen_kernel(const __g
             Servers srv{P.n_servers ? P.n_servers : 1u, L.srv + (size_t)blockIdx.x * blockDim.x + tid,
                         (uint32_t)gstride};
             for (uint32_t q = 0; q < srv.S; ++q) srv.V[(size_t)q * srv.stride] = 0.0;
-            for (uint32_t x = 0; x < nbt; ++x)
-              dispatch<true>(R, srv, ovS[(size_t)x * gstride], ovM[(size_t)x * gstride]);
+            for (uint32_t x = 0; x < nbt; ++x) {
+              const double fin = dispatch<true>(R, srv, ovS[(size_t)x * gstride], ovM[(size_t)x * gstride]);
+              if (Q) {  // the batch list now holds completions
+                ovS[(size_t)x * gstride] = fin;
+                q.lmin = fmin(q.lmin, fin);
+                q.lmax = fmax(q.lmax, fin);
+              }
+            }
             busy = R.busy;
             latw = R.latw;
             mk = R.D;
+          } else if (Q) {  // one server: completions are the running sum in dispatch order
+            double D = 0.0;
+            for (uint32_t x = 0; x < nbt; ++x) {
+              D = __dadd_rn(D, ovS[(size_t)x * gstride]);
+              ovS[(size_t)x * gstride] = D;
+              q.lmin = fmin(q.lmin, D);
+              q.lmax = fmax(q.lmax, D);
+            }
           }
           if (nc > 0) {
             mk_out = mk;
             thr_out = (double)nc / mk_out;
             busy_out = busy / ((double)(MS && P.n_servers ? P.n_servers : 1u) * mk_out);
             lat_out = latw / (double)nc;
+            q_ok = Q;
+            q_m = nc;
+            q_nb = nbt;
           } else {
             mk_out = thr_out = busy_out = lat_out = 0.0;
           }
@@ -513,11 +626,47 @@ __global__ void __launch_bounds__(kGenThreads, BB_GEN_MINB) gen_kernel(const __g
           mk_out = thr_out = busy_out = lat_out = BB_QNAN;
         }
       }
+      // no completed request: finish() leaves the defaults (0); failed: NaN
+      if (!failed && !q_ok) q_p50 = q_p99 = 0.0;
+    }
+    if (Q && BB_QSTAGE >= 3) {  // the warp selects each of its replications' p50/p99 in turn
+      uint32_t pend = __ballot_sync(kQFull, q_ok);
+      while (pend) {
+        const uint32_t l = __ffs(pend) - 1;
+        pend &= pend - 1;
+        const uint64_t m = __shfl_sync(kQFull, q_m, l);
+        const double lmin = __shfl_sync(kQFull, q.lmin, l), lmax = __shfl_sync(kQFull, q.lmax, l);
+        const size_t ls = (size_t)blockIdx.x * kGenThreads + wib * 32 + l;
+        double v50, v99;
+        if (!OVL) {
+          const uint32_t ncl = __shfl_sync(kQFull, q.nc, l);
+          double* A_l = L.qA + qwarp * L.q_n * 32 + l * 32;
+          QSrcLogRev first{A_l, L.qB + qwarp * L.q_n * 32 + l * 32, L.qF + qwarp * L.q_nf * 32 + l,
+                           L.qP + qwarp * kmax * 32 + l, q_carry, n, ncl, k, lane, 0.0};
+          const QSrcLat rest{A_l, n, lane};
+          q_select(first, rest, m, lmin, lmax, wreg, qregion, q_ans, lane, v50, v99);
+          double sum = first.sum;  // latency_mean from the latencies themselves
+#pragma unroll
+          for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(kQFull, sum, o);
+          if (lane == l) lat_out = sum / (double)m;
+        } else {
+          const uint32_t nb = __shfl_sync(kQFull, q_nb, l);
+          QSrcBatches src{L.ovS + ls, L.ovM + ls, gstride, nb, lane};
+          q_select(src, src, m, lmin, lmax, wreg, qregion, q_ans, lane, v50, v99);
+        }
+        if (lane == l) {
+          q_p50 = v50;
+          q_p99 = v99;
+        }
+      }
+    }
+    if (r < L.rep_end) {
       const uint64_t o = (uint64_t)P.gidx * L.reps_total + r;
       L.out[BB_REP_THROUGHPUT * stride + o] = thr_out;
       L.out[BB_REP_LATENCY * stride + o] = lat_out;
-      L.out[BB_REP_P50 * stride + o] = BB_QNAN;  // generated mode: not tracked (SURVEY §7 hard part 4)
-      L.out[BB_REP_P99 * stride + o] = BB_QNAN;
+      // without quantile mode p50/p99 are not tracked (NaN)
+      L.out[BB_REP_P50 * stride + o] = Q ? q_p50 : BB_QNAN;
+      L.out[BB_REP_P99 * stride + o] = Q ? q_p99 : BB_QNAN;
       L.out[BB_REP_MAKESPAN * stride + o] = mk_out;
       L.out[BB_REP_BUSY * stride + o] = busy_out;
     }
@@ -527,12 +676,10 @@ __global__ void __launch_bounds__(kGenThreads, BB_GEN_MINB) gen_kernel(const __g
 
 
 
-template <int SVC, int ERR, bool OVL, bool TRACK, bool MS = false>
+template <int SVC, int ERR, bool OVL, bool TRACK, bool MS, bool Q>
 cudaError_t launch_gen(const GenLaunch& L, cudaStream_t s) {
-  // packed state (+ open arrival sums without flush | + overload tables)
-  const size_t per = OVL ? (8 + 16) : (TRACK ? 16 : 8);
-  const size_t smem = (size_t)L.k_max * kGenThreads * per;
-  auto kern = gen_kernel<SVC, ERR, OVL, TRACK, MS>;
+  const size_t smem = (size_t)gen_warp_bytes(L.k_max, OVL, TRACK, Q) * kGenWarps;
+  auto kern = gen_kernel<SVC, ERR, OVL, TRACK, MS, Q>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 0, occ = 0;
@@ -549,39 +696,78 @@ cudaError_t launch_gen(const GenLaunch& L, cudaStream_t s) {
   if (grid == 0) return cudaSuccess;
   GenLaunch L2 = L;
   double* srv = nullptr;
-  unsigned char* ovl = nullptr;
-  if (OVL && MS) {  // per-thread batch list (service, members): bound the scratch to 4 GiB
-    const uint64_t per_thread = (uint64_t)L.nb_max * (sizeof(double) + sizeof(uint16_t));
-    const uint64_t max_grid = ((uint64_t)4 << 30) / (per_thread * kGenThreads);
+  // per-resident-thread HBM scratch: overload batch lists (S > 1 servers or
+  // quantile mode), the finite-rate request log (quantile mode)
+  const bool blist = OVL && (MS || Q), rlog = Q && !OVL;
+  const uint64_t q_n = rlog ? ((uint64_t)L.n_max + 31) & ~31ull : 0, q_nf = rlog ? L.nf_max : 0;
+  const uint64_t per_thread = (blist ? (uint64_t)L.nb_max * (sizeof(double) + sizeof(uint16_t)) : 0) +
+                              (rlog ? q_n * 9 + (q_nf + L.k_max) * sizeof(double) : 0);
+  bool held = false;
+  if (per_thread) {
+    // quantile mode may use most of HBM (a 10^5-request log is 0.9 MB per
+    // thread); the S > 1 batch lists alone stay within 4 GiB as before
+    const uint64_t budget = Q ? gen_scratch_budget() : ((uint64_t)4 << 30);
+    const uint64_t max_grid = budget / ((per_thread + 1024) * kGenThreads);
     if (max_grid == 0) return cudaErrorMemoryAllocation;
     grid = (unsigned)(grid < max_grid ? grid : max_grid);
-    const size_t cnt = (size_t)grid * kGenThreads * L.nb_max;
-    e = cudaMallocAsync((void**)&ovl, cnt * (sizeof(double) + sizeof(uint16_t)), s);
+    const uint64_t slots = (uint64_t)grid * kGenThreads;
+    const uint64_t nbl = blist ? slots * L.nb_max : 0;
+    const uint64_t bytes = nbl * (sizeof(double) + sizeof(uint16_t)) + slots * (q_n * 9 + (q_nf + L.k_max) * 8) + 1024;
+    unsigned char* base = nullptr;
+    e = gen_scratch_acquire(bytes, s, reinterpret_cast<void**>(&base));
     if (e != cudaSuccess) return e;
-    L2.ovS = reinterpret_cast<double*>(ovl);
-    L2.ovM = reinterpret_cast<uint16_t*>(ovl + cnt * sizeof(double));
+    held = true;
+    // doubles first, then u16, then bytes (alignment)
+    size_t off = 0;
+    auto carve = [&](size_t b) {
+      unsigned char* p = base + off;
+      off += (b + 255) & ~(size_t)255;
+      return p;
+    };
+    if (blist) L2.ovS = reinterpret_cast<double*>(carve(nbl * sizeof(double)));
+    if (rlog) {
+      L2.qA = reinterpret_cast<double*>(carve(slots * q_n * sizeof(double)));
+      L2.qF = reinterpret_cast<double*>(carve(slots * q_nf * sizeof(double)));
+      L2.qP = reinterpret_cast<double*>(carve(slots * L.k_max * sizeof(double)));
+    }
+    if (blist) L2.ovM = reinterpret_cast<uint16_t*>(carve(nbl * sizeof(uint16_t)));
+    if (rlog) L2.qB = reinterpret_cast<uint8_t*>(carve(slots * q_n));
+    L2.q_n = q_n;
+    L2.q_nf = q_nf;
   }
   if (L.s_max > 1) {  // free times of S servers per resident thread
     e = cudaMallocAsync((void**)&srv, (size_t)grid * kGenThreads * L.s_max * sizeof(double), s);
-    if (e != cudaSuccess) return e;
+    if (e != cudaSuccess) {
+      if (held) gen_scratch_release(s);
+      return e;
+    }
     L2.srv = srv;
   }
   kern<<<grid, kGenThreads, smem, s>>>(L2);
   note_launch();
   e = cudaGetLastError();
   if (srv) cudaFreeAsync(srv, s);
-  if (ovl) cudaFreeAsync(ovl, s);
+  if (held) gen_scratch_release(s);
   return e;
+}
+
+template <int SVC, int ERR, bool Q>
+cudaError_t launch_mode_q(const GenLaunch& L, cudaStream_t s) {
+  if (L.overload)
+    return L.s_max > 1 ? launch_gen<SVC, ERR, true, false, true, Q>(L, s)
+                       : launch_gen<SVC, ERR, true, false, false, Q>(L, s);
+  // S > 1 servers: finite rates only (validated on the host); leftover sums kept
+  // (quantile mode sums the latencies themselves: no open arrival sums)
+  if (L.s_max > 1) return launch_gen<SVC, ERR, false, !Q, true, Q>(L, s);
+  if constexpr (!Q) {
+    if (L.track) return launch_gen<SVC, ERR, false, true, false, Q>(L, s);
+  }
+  return launch_gen<SVC, ERR, false, false, false, Q>(L, s);
 }
 
 template <int SVC, int ERR>
 cudaError_t launch_mode(const GenLaunch& L, cudaStream_t s) {
-  if (L.overload)
-    return L.s_max > 1 ? launch_gen<SVC, ERR, true, false, true>(L, s)
-                       : launch_gen<SVC, ERR, true, false>(L, s);
-  // S > 1 servers: finite rates only (validated on the host); leftover sums kept
-  if (L.s_max > 1) return launch_gen<SVC, ERR, false, true, true>(L, s);
-  return L.track ? launch_gen<SVC, ERR, false, true>(L, s) : launch_gen<SVC, ERR, false, false>(L, s);
+  return L.quant ? launch_mode_q<SVC, ERR, true>(L, s) : launch_mode_q<SVC, ERR, false>(L, s);
 }
 
 template <int SVC>

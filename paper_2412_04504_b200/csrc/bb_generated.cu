@@ -1,6 +1,8 @@
 // bb_generated.cu -- generated-mode host entry points: key-space threshold
 // setup, the per-family kernel dispatch (bb_gen_kernel.cuh) and the
 // per-point replica reduction.
+#include <mutex>
+
 #include "bb_generated.cuh"
 
 namespace bb {
@@ -99,6 +101,57 @@ __global__ void point_reduce_kernel(const double* __restrict__ rep, uint32_t n_p
 }
 
 }  // namespace
+
+namespace {
+struct Scratch {
+  std::mutex mu;
+  void* p = nullptr;
+  size_t bytes = 0;
+  cudaEvent_t ev = nullptr;
+};
+Scratch g_scratch[64];
+int cur_dev() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d & 63;
+}
+}  // namespace
+
+cudaError_t gen_scratch_acquire(size_t bytes, cudaStream_t s, void** out) {
+  Scratch& S = g_scratch[cur_dev()];
+  S.mu.lock();
+  cudaError_t e = cudaSuccess;
+  if (!S.ev) e = cudaEventCreateWithFlags(&S.ev, cudaEventDisableTiming);
+  else e = cudaStreamWaitEvent(s, S.ev, 0);
+  if (e == cudaSuccess && bytes > S.bytes) {
+    if (S.p) cudaFree(S.p);  // synchronises: earlier users are done
+    S.p = nullptr;
+    S.bytes = 0;
+    e = cudaMalloc(&S.p, bytes);
+    if (e == cudaSuccess) S.bytes = bytes;
+    else S.p = nullptr;
+  }
+  if (e != cudaSuccess) {
+    S.mu.unlock();
+    return e;
+  }
+  *out = S.p;
+  return cudaSuccess;
+}
+
+void gen_scratch_release(cudaStream_t s) {
+  Scratch& S = g_scratch[cur_dev()];
+  cudaEventRecord(S.ev, s);
+  S.mu.unlock();
+}
+
+uint64_t gen_scratch_budget() {
+  size_t free_b = 0, total_b = 0;
+  if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) return 0;
+  const uint64_t have = free_b + g_scratch[cur_dev()].bytes;
+  const uint64_t reserve = (uint64_t)8 << 30;  // leave room for the caller's own tensors
+  return have > reserve ? (uint64_t)((have - reserve) * 0.85) : 0;
+}
 
 cudaError_t gen_setup_thresholds(GenPoint* pts_dev, uint32_t n_points, cudaStream_t s) {
   if (!n_points) return cudaSuccess;

@@ -52,7 +52,23 @@ struct GenLaunch {
   double* ovS;              // overload, S > 1: per-thread batch services (set by gen_run)
   uint16_t* ovM;            //   ... and member counts
   DevError* err;
+  // quantile mode (bb_quantile.cuh): exact per-replication p50/p99
+  int32_t quant;
+  uint32_t n_max;           // most requests of any point in the launch
+  uint32_t nf_max;          // most full batches of any point (n/B + 1)
+  double* qA;               // request log per resident thread [slot][q_n] (set by gen_run)
+  uint8_t* qB;              //   (bin | closed) bytes [slot][q_n]
+  double* qF;               //   full-batch completions [slot][q_nf]
+  double* qP;               //   per-bin first arrival / partial completion [slot][k_max]
+  uint64_t q_n, q_nf;
 };
+
+// Grow-only per-device HBM scratch of the fused kernel, reused in stream
+// order (acquire waits for the previous user's work; release records it).
+cudaError_t gen_scratch_acquire(size_t bytes, cudaStream_t s, void** out);
+void gen_scratch_release(cudaStream_t s);
+// Bytes the scratch may grow to (free HBM + what it already holds, less a reserve).
+uint64_t gen_scratch_budget();
 
 // Resolves key-space thresholds (bisection on the device sampler).
 cudaError_t gen_setup_thresholds(GenPoint* pts_dev, uint32_t n_points, cudaStream_t s);

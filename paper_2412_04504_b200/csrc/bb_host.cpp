@@ -25,6 +25,9 @@
 namespace bb {
 static std::atomic<unsigned long long> g_launches{0};
 static std::atomic<unsigned long long> g_h2d{0}, g_d2h{0};
+// generated mode: exact per-replication p50/p99 (the reference always computes
+// them, simulator.hpp:289-301); off only for A/B measurements
+static std::atomic<int> g_gen_quantiles{1};
 void note_launch(unsigned n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 }  // namespace bb
 
@@ -952,7 +955,7 @@ void launch_sweep(const SweepParams* E, Sweep& W, uint64_t rep_begin, uint64_t r
   for (size_t i = 0; i < P; ++i) {
     if (done[i]) continue;
     std::vector<uint32_t> members;
-    uint32_t kmax = 1, smax = 1;
+    uint32_t kmax = 1, smax = 1, nmax = 1, nfmax = 1;
     uint64_t nbmax = 1;
     for (size_t j = i; j < P; ++j)
       if (!done[j] && keys[j].err == keys[i].err && keys[j].cyc == keys[i].cyc &&
@@ -963,6 +966,8 @@ void launch_sweep(const SweepParams* E, Sweep& W, uint64_t rep_begin, uint64_t r
         kmax = std::max(kmax, W.gp[j].k);
         smax = std::max(smax, W.gp[j].n_servers);
         nbmax = std::max<uint64_t>(nbmax, W.gp[j].n / W.gp[j].B + W.gp[j].k + 1);
+        nmax = std::max(nmax, W.gp[j].n);
+        nfmax = std::max(nfmax, W.gp[j].n / W.gp[j].B + 1);
       }
     const bb::GenPoint* base = W.d_pts.as<bb::GenPoint>();
     DBuf grp;
@@ -994,6 +999,9 @@ void launch_sweep(const SweepParams* E, Sweep& W, uint64_t rep_begin, uint64_t r
     L.track = keys[i].track;
     L.overload = keys[i].ovl;
     L.out = rep_dev;
+    L.quant = bb::g_gen_quantiles.load() ? 1 : 0;
+    L.n_max = nmax;
+    L.nf_max = nfmax;
     DBuf err(sizeof(bb::DevError), st);
     CK(cudaMemsetAsync(err.p, 0xFF, 8, st));
     L.err = err.as<bb::DevError>();
@@ -1372,6 +1380,8 @@ void bb_transfer_bytes(uint64_t* h2d_bytes, uint64_t* d2h_bytes, int reset) {
   if (h2d_bytes) *h2d_bytes = reset ? bb::g_h2d.exchange(0) : bb::g_h2d.load();
   if (d2h_bytes) *d2h_bytes = reset ? bb::g_d2h.exchange(0) : bb::g_d2h.load();
 }
+
+int bb_set_generated_quantiles(int on) { return bb::g_gen_quantiles.exchange(on ? 1 : 0); }
 
 uint64_t bb_launch_count(int reset) {
   return reset ? bb::g_launches.exchange(0) : bb::g_launches.load();
