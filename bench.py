@@ -41,6 +41,11 @@ SEED = 0x0000000241204504
 METRIC = "simulated requests/s (MBB k×B×λ sweep) at 1/2/4/8 B200 vs CPU ref"
 ALG_INSTR_BASE = 132.0  # lane-instructions per request, base case
 ALG_INSTR_PER_BATCH = 12.0
+# exact per-replication p50/p99 (the reference sorts every replication's
+# latencies, simulator.hpp:289-301): the fused kernel logs (arrival fp64,
+# batch id u32) per request and reads the log back once -- 24 B/request of
+# HBM traffic that no log-based exact selection avoids
+ALG_BYTES_QUANTILES = 24.0
 
 
 def measured_peaks():
@@ -200,6 +205,9 @@ def workload_config(args, reps):
         "requests_per_replication": args.requests,
         "requests_per_step_per_gpu": len(KS) * len(BS) * len(FRACS) * reps * args.requests,
         "rng": "Philox4x32-10 (counter-based), fp64 arrival clock and Lindley recursion",
+        "quantiles": ("off (A/B run)" if getattr(args, "no_quantiles", False) else
+                      "exact latency p50/p99 of every replication, averaged per point, as "
+                      "run_point does (experiment.hpp:256-279)"),
         "l2": "no HBM-resident inputs in generated mode; a 512 MiB buffer is written between "
               "timed steps anyway (L2 flushed)",
         "parallelism": f"replicas sharded over {args.gpus} GPU(s), 1 NCCL all-reduce per step",
@@ -220,6 +228,7 @@ def main():
     ap.add_argument("--no-trace", action="store_true")
     ap.add_argument("--no-quantiles", action="store_true",
                     help="A/B only: skip the per-replication p50/p99 the reference computes")
+    ap.add_argument("--no-ab", action="store_true", help="skip the without-quantiles A/B leg")
     ap.add_argument("--dist-backend", default="nccl", help="nccl (default) or gloo for testing")
     args = ap.parse_args()
     if args.impl == "reference":
@@ -336,25 +345,46 @@ def main():
     instr = alg_instr(pts, R)
     sm_mhz = ck.get("sm_mhz") or 1327.0
     peak = 148 * 4 * 32 * sm_mhz * 1e6
+    peaks = measured_peaks()
+    hbm_peak = float(peaks.get("hbm_gbs") or peaks.get("hbm_copy_gbs") or 6650.0) * 1e9
+    quant = not args.no_quantiles
     roofline = None
     if kernel_ms:
-        achieved = instr / (kernel_ms / 1e3)
+        # two floors on one kernel: the simulation's instruction issue and,
+        # with the quantiles, the request log's HBM traffic
+        t_k = kernel_ms / 1e3
+        t_issue = instr / peak
+        qbytes = ALG_BYTES_QUANTILES * requests_step if quant else 0.0
+        t_hbm = qbytes / hbm_peak
         traffic = None
-        prof = os.path.join(ROOT, "profiles", "r01_gen_kernel_ncu.json")
-        if os.path.exists(prof):  # one `ncu --set full` capture at 1500 replications/point
+        prof = os.path.join(ROOT, "profiles", "r01_gen_kernel_q_ncu.json" if quant
+                            else "r01_gen_kernel_ncu.json")
+        if os.path.exists(prof):  # one `ncu --set full` capture; scaled per launch
             cap = json.load(open(prof))
             cap = cap[0] if isinstance(cap, list) else cap
-            if cap.get("dram_bytes_per_launch") is not None:
+            if cap.get("dram_bytes_per_request") is not None:
+                traffic = cap["dram_bytes_per_request"] * requests_step
+            elif cap.get("dram_bytes_per_launch") is not None:
                 traffic = cap["dram_bytes_per_launch"] * R / 1500.0
+        hbm_dom = t_hbm > t_issue
         roofline = {
-            "bound": "issue", "kernel": "gen_kernel",
-            "achieved": achieved / 1e9, "peak": peak / 1e9, "unit": "Glane-instr/s",
-            "frac": achieved / peak, "traffic": traffic,
+            "bound": "hbm" if hbm_dom else "issue", "kernel": "gen_kernel",
+            "achieved": (qbytes / t_k / 1e9) if hbm_dom else instr / t_k / 1e9,
+            "peak": hbm_peak / 1e9 if hbm_dom else peak / 1e9,
+            "unit": "GB/s" if hbm_dom else "Glane-instr/s",
+            "frac": max(t_issue, t_hbm) / t_k, "traffic": traffic,
+            "issue": {"achieved": instr / t_k / 1e9, "peak": peak / 1e9, "unit": "Glane-instr/s",
+                      "frac": t_issue / t_k},
+            "hbm": {"achieved": qbytes / t_k / 1e9, "peak": hbm_peak / 1e9, "unit": "GB/s",
+                    "frac": t_hbm / t_k},
             "kernel_ms": kernel_ms, "kernel_share_of_step": kernel_ms / (total_ms / args.steps),
-            "algorithmic": f"{ALG_INSTR_BASE:.0f} + {ALG_INSTR_PER_BATCH:.0f}/B lane-instructions "
-                           "per request (SURVEY 8d base case) x requests per launch",
-            "peak_basis": f"148 SM x 4 schedulers x 32 lanes x {sm_mhz} MHz (median SM clock "
-                          "during the timed region)",
+            "algorithmic": f"issue: {ALG_INSTR_BASE:.0f} + {ALG_INSTR_PER_BATCH:.0f}/B lane-instructions "
+                           "per request (SURVEY 8d base case); hbm: "
+                           + (f"{ALG_BYTES_QUANTILES:.0f} B/request (exact p50/p99: write + read the "
+                              "12 B request log)" if quant else "none (quantiles off)")
+                           + "; frac = max(issue time, HBM time) at peak / kernel time",
+            "peak_basis": f"issue: 148 SM x 4 schedulers x 32 lanes x {sm_mhz} MHz (median SM "
+                          "clock during the timed region); hbm: MEASURED_PEAKS.json",
         }
     line = {
         "metric": METRIC, "value": value, "unit": "requests/s", "n_gpus": world,
@@ -368,6 +398,27 @@ def main():
                          "throughput_mean": results["pts"][-1].throughput_mean,
                          "latency_mean": results["pts"][-1].latency_mean},
     }
+    if world == 1 and quant and not args.no_ab:
+        # A/B only: the same sweep without the per-replication quantiles
+        bb.set_generated_quantiles(False)
+        try:
+            step()
+            torch.cuda.synchronize()
+            ab = []
+            for _ in range(2):
+                flush.fill_(1)
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                step()
+                e1.record(stream)
+                torch.cuda.synchronize()
+                ab.append(e0.elapsed_time(e1))
+            line["without_quantiles"] = {
+                "value": requests_step * len(ab) / (sum(ab) / 1e3), "unit": "requests/s",
+                "note": "A/B only: p50/p99 left NaN, i.e. less work than the reference's run_point"}
+        finally:
+            bb.set_generated_quantiles(True)
     if world == 1 and not args.no_trace:
         try:
             line["trace"] = trace_measure(bb, torch, dev, stream)

@@ -109,7 +109,7 @@ struct Servers {
 // step D = max(D, R) + S, and D is also the last completion).
 // MS selects the S-server code at compile time so that the one-server kernel
 // keeps its register budget (128 regs, 16 warps/SM).
-template <bool MS>
+template <bool MS, bool LAT = true>
 __device__ __forceinline__ double dispatch(Rep& R, const Servers& sv, double S, uint32_t members) {
   double fin;
   if (!MS) {
@@ -129,7 +129,7 @@ __device__ __forceinline__ double dispatch(Rep& R, const Servers& sv, double S, 
     R.D = fmax(R.D, fin);  // last completion (simulator.hpp:275)
   }
   R.busy += S;
-  R.latw += (double)members * fin;
+  if (LAT) R.latw += (double)members * fin;  // (quantile mode sums the latencies themselves)
   R.ncomp += members;
   return fin;
 }
@@ -137,32 +137,38 @@ __device__ __forceinline__ double dispatch(Rep& R, const Servers& sv, double S, 
 // Quantile mode (bb_quantile.cuh): the forward pass's request log, this
 // lane's view of its warp's interleaved rows (layout in bb_quantile.cuh).
 struct QLog {
-  double* A;       // arrival of request i at A[(i/32)*1024 + i%32]
-  uint8_t* Bf;     // (bin - 1) | closed << 7 at Bf[(i/32)*1024 + i%32]
-  double* F;       // completion of full batch c (closing order) at F[c*32]
-  double* P;       // per bin: the drained partial's completion (NaN: none) at P[b*32]
-  uint32_t nc;     // full batches closed
-  double lmin, lmax;
+  double* A;       // arrival of request i at A[qlog_index(i)]
+  uint32_t* Id;    // its batch id, same layout
+  double* F;       // completion of batch id q at F[q] (this lane's row)
+  uint32_t nb;     // batch ids issued
+  double* lm;      // shared: [0] a lower bound of the latencies, [32] an upper bound
 };
 
 // One request folded into its bin; closes the batch at B members
 // (on_arrival + form_batch, simulator.hpp:187-254).  Returns 1 when it closed.
+// Quantile mode: osum holds the bin's previous closing time, bid its open
+// batch's id; *id receives the request's batch id.
 template <int SVC, bool track, bool MS, bool Q>
 __device__ __forceinline__ uint32_t fold(Rep& R, uint64_t* __restrict__ slot, double* __restrict__ osum,
-                                         uint64_t xs, uint32_t B, const SvcParams& svc,
-                                         const Servers& sv, QLog& q, uint32_t b) {
+                                         uint32_t* __restrict__ bid, uint64_t xs, uint32_t B,
+                                         const SvcParams& svc, const Servers& sv, QLog& q,
+                                         uint32_t& id) {
   const uint64_t s0 = *slot;
   const uint64_t km = max(s0 & ~kCntMask, xs << kCntBits);
   const uint32_t cnt = (uint32_t)(s0 & kCntMask) + 1;
+  if (Q) {
+    id = cnt == 1 ? q.nb++ : *bid;  // the first member opens a batch
+    if (cnt == 1 && cnt != B) *bid = id;
+  }
   if (cnt == B) {
     *slot = 0;
-    const double fin = dispatch<MS>(R, sv, svc_of_key_t<SVC>(svc, km >> kCntBits), B);
+    const double fin = dispatch<MS, !Q>(R, sv, svc_of_key_t<SVC>(svc, km >> kCntBits), B);
     if (track) *osum = 0.0;
-    if (Q) {  // osum is the bin's previous closing time in quantile mode
-      q.F[(size_t)(q.nc++) * 32] = fin;
+    if (Q) {
+      q.F[id] = fin;
       const double lo = __dsub_rn(fin, R.t), hi = __dsub_rn(fin, *osum);
-      q.lmin = lo < q.lmin ? lo : q.lmin;  // closing member: the batch's smallest latency
-      q.lmax = hi > q.lmax ? hi : q.lmax;  // bounds the first member's (it arrived later)
+      if (lo < q.lm[0]) q.lm[0] = lo;    // closing member: the batch's smallest latency
+      if (hi > q.lm[32]) q.lm[32] = hi;  // bounds the first member's (it arrived later)
       *osum = R.t;
     }
     return 1u;
@@ -172,6 +178,9 @@ __device__ __forceinline__ uint32_t fold(Rep& R, uint64_t* __restrict__ slot, do
   return 0u;
 }
 
+#ifndef BB_QWRITE
+#define BB_QWRITE 1  // 1: the first selection pass writes the latencies for the later ones
+#endif
 #ifndef BB_QSTAGE
 #define BB_QSTAGE 3  // A/B only: 1 = request log, 2 = + latencies, 3 = + selection
 #endif
@@ -186,13 +195,15 @@ __device__ __forceinline__ uint32_t fold(Rep& R, uint64_t* __restrict__ slot, do
 #endif
 // shared bytes of one warp's state rows, and of its whole region
 // (quantile mode, finite rate: the second row set holds each bin's previous
-// closing time instead of the open arrival sums)
+// closing time instead of the open arrival sums, a third (u32) its open
+// batch's id)
 __host__ __device__ __forceinline__ uint32_t gen_state_bytes(uint32_t kmax, bool ovl, bool track, bool q) {
-  return kmax * 256u * (ovl ? 3u : ((track || q) ? 2u : 1u));
+  if (ovl) return kmax * 768u;
+  return q ? kmax * 640u + 512u : kmax * 256u * (track ? 2u : 1u);
 }
 __host__ __device__ __forceinline__ uint32_t gen_warp_bytes(uint32_t kmax, bool ovl, bool track, bool q) {
   const uint32_t st = gen_state_bytes(kmax, ovl, track, q);
-  return q ? (st > kQRegionMin ? st : kQRegionMin) + kmax * 8u + 32u : st;
+  return q ? (st > kQRegionMin ? st : kQRegionMin) + 32u : st;
 }
 
 template <int SVC, int ERR, bool OVL, bool TRACK, bool MS, bool Q>
@@ -216,10 +227,10 @@ __global__ void __launch_bounds__(kGenThreads, Q ? 2 : BB_GEN_MINB) gen_kernel(c
   uint32_t* s_rem = s_F + (size_t)kmax * 32;
   uint32_t* s_cf = s_rem + (size_t)kmax * 32;
   uint32_t* s_jd = s_cf + (size_t)kmax * 32;
+  uint32_t* s_bid = reinterpret_cast<uint32_t*>(st + (size_t)kmax * 64);  // quantile mode
   const uint32_t qregion = gen_state_bytes(kmax, OVL, TRACK, Q) > kQRegionMin
                                ? gen_state_bytes(kmax, OVL, TRACK, Q) : kQRegionMin;
-  double* q_carry = reinterpret_cast<double*>(wreg + qregion);  // [kmax]
-  double* q_ans = q_carry + kmax;                                  // [4]
+  double* q_ans = reinterpret_cast<double*>(wreg + qregion);  // [4]
 
   const uint32_t nrep = L.rep_end - L.rep_begin;
   const uint32_t chunks = (nrep + 31) / 32;
@@ -240,7 +251,8 @@ __global__ void __launch_bounds__(kGenThreads, Q ? 2 : BB_GEN_MINB) gen_kernel(c
     // quantile mode: this lane's request log and what the warp's selection needs
     const size_t qslot = (size_t)blockIdx.x * kGenThreads + tid;
     const size_t qwarp = (size_t)blockIdx.x * kGenWarps + wib;
-    QLog q{nullptr, nullptr, nullptr, nullptr, 0u, CUDART_INF, 0.0};
+    QLog q{nullptr, nullptr, nullptr, 0u, nullptr};
+    double q_lmin = CUDART_INF, q_lmax = 0.0;  // (overload: bounds of the batch completions)
     bool q_ok = false;
     uint64_t q_m = 0;
     uint32_t q_nb = 0;
@@ -307,10 +319,12 @@ __global__ void __launch_bounds__(kGenThreads, Q ? 2 : BB_GEN_MINB) gen_kernel(c
           for (uint32_t b = 0; b < k; ++b) s_osum[b * 32 + lane] = 0.0;
         Rep R{0.0, 0.0, 0.0, 0.0, 0.0, 0};
         if (Q) {
-          q.A = L.qA + qwarp * L.q_n * 32 + lane * 32;
-          q.Bf = L.qB + qwarp * L.q_n * 32 + lane * 32;
-          q.F = L.qF + qwarp * L.q_nf * 32 + lane;
-          q.P = L.qP + qwarp * kmax * 32 + lane;
+          q.A = L.qA + qwarp * L.q_n * 32 + lane * kQRun;
+          q.Id = L.qI + qwarp * L.q_n * 32 + lane * kQRun;
+          q.F = L.qF + qslot * L.q_nf;
+          q.lm = reinterpret_cast<double*>(s_bid + (size_t)kmax * 32) + lane;
+          q.lm[0] = CUDART_INF;
+          q.lm[32] = 0.0;
         }
         Servers srv{MS && P.n_servers ? P.n_servers : 1u, nullptr, 0};
         if (MS && srv.S > 1) {  // all servers idle at t = 0
@@ -323,7 +337,7 @@ __global__ void __launch_bounds__(kGenThreads, Q ? 2 : BB_GEN_MINB) gen_kernel(c
         // U requests per iteration: their draws, exponentials and bins are
         // independent, so the latencies overlap; the folds stay in order
         constexpr int U = BB_GEN_UNROLL;
-        static_assert(!Q || U % 4 == 0, "the request log packs 4 requests per lane");
+        static_assert(!Q || (U % 4 == 0 && kQRun % 4 == 0), "the request log packs 4 requests per lane");
         // software pipeline: the next group's Philox blocks (integer pipes)
         // are issued in the same basic block as this group's exponentials
         // (fp64 pipe) so the scheduler interleaves them (cyclic traces keep a
@@ -385,29 +399,24 @@ __global__ void __launch_bounds__(kGenThreads, Q ? 2 : BB_GEN_MINB) gen_kernel(c
             for (int u = 0; u < U; ++u)
               pb[u] = pred_of(BK ? bin_bkt(bkt, bshift, d[u].xs)
                                  : bin_of(thr, bkt, false, bshift, k, top, d[u].xs), e[u]);
-            uint32_t cl[U];
+            uint32_t qid[U];
             double at[U];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
               R.t = __dadd_rn(R.t, g[u]);  // exponential inter-arrival, simulator.hpp:181 (no contraction)
-              R.asum += R.t;
+              if (!Q) R.asum += R.t;
               at[u] = R.t;
-              cl[u] = fold<SVC, TRACK, MS, Q>(R, st + (pb[u] - 1) * 32 + lane,
-                                              s_osum + (pb[u] - 1) * 32 + lane, d[u].xs, B, svc,
-                                              srv, q, pb[u] - 1);
+              fold<SVC, TRACK, MS, Q>(R, st + (pb[u] - 1) * 32 + lane, s_osum + (pb[u] - 1) * 32 + lane,
+                                      s_bid + (pb[u] - 1) * 32 + lane, d[u].xs, B, svc, srv, q, qid[u]);
             }
-            if (Q) {  // request log: arrivals (16 B stores) and (bin | closed) bytes
+            if (Q) {  // request log: arrivals and batch ids (16 B stores)
+              const size_t o = qlog_index(i);  // (i % 4 == 0: 4 requests stay in one run)
 #pragma unroll
               for (int u = 0; u < U; u += 2)
-                *reinterpret_cast<double2*>(q.A + (size_t)((i + u) >> 5) * 1024 + ((i + u) & 31)) =
-                    make_double2(at[u], at[u + 1]);
+                *reinterpret_cast<double2*>(q.A + o + u) = make_double2(at[u], at[u + 1]);
 #pragma unroll
-              for (int u = 0; u < U; u += 4) {
-                uint32_t w4 = 0;
-#pragma unroll
-                for (int v = 0; v < 4 && u + v < U; ++v) w4 |= ((pb[u + v] - 1) | (cl[u + v] << 7)) << (8 * v);
-                *reinterpret_cast<uint32_t*>(q.Bf + (size_t)((i + u) >> 5) * 1024 + ((i + u) & 31)) = w4;
-              }
+              for (int u = 0; u < U; u += 4)
+                *reinterpret_cast<uint4*>(q.Id + o + u) = make_uint4(qid[u], qid[u + 1], qid[u + 2], qid[u + 3]);
             }
             if (PIPE) {
 #pragma unroll
@@ -432,13 +441,13 @@ __global__ void __launch_bounds__(kGenThreads, Q ? 2 : BB_GEN_MINB) gen_kernel(c
           } else {
             const uint32_t p0 = bin_pred(d0.xs, e0);
             R.t = __dadd_rn(R.t, __dmul_rn(exp1_tab(d0.xg, s_logtab), inv_lambda));
-            R.asum += R.t;
-            const uint32_t c0 = fold<SVC, TRACK, MS, Q>(R, st + (p0 - 1) * 32 + lane,
-                                                        s_osum + (p0 - 1) * 32 + lane, d0.xs, B,
-                                                        svc, srv, q, p0 - 1);
+            if (!Q) R.asum += R.t;
+            uint32_t id0 = 0;
+            fold<SVC, TRACK, MS, Q>(R, st + (p0 - 1) * 32 + lane, s_osum + (p0 - 1) * 32 + lane,
+                                    s_bid + (p0 - 1) * 32 + lane, d0.xs, B, svc, srv, q, id0);
             if (Q) {
-              q.A[(size_t)(i >> 5) * 1024 + (i & 31)] = R.t;
-              q.Bf[(size_t)(i >> 5) * 1024 + (i & 31)] = (uint8_t)((p0 - 1) | (c0 << 7));
+              q.A[qlog_index(i)] = R.t;
+              q.Id[qlog_index(i)] = id0;
             }
           }
         }
@@ -447,21 +456,18 @@ __global__ void __launch_bounds__(kGenThreads, Q ? 2 : BB_GEN_MINB) gen_kernel(c
           for (uint32_t b = 0; b < k; ++b) {
             const uint64_t s0 = st[b * 32 + lane];
             const uint32_t cnt = (uint32_t)(s0 & kCntMask);
-            if (!cnt) {
-              if (Q) q.P[b * 32] = BB_QNAN;
-              continue;
-            }
+            if (!cnt) continue;
             if (flush) {  // on_drain partials at the last arrival, bin order
-              const double fin = dispatch<MS>(R, srv, svc_of_key_t<SVC>(svc, s0 >> kCntBits), cnt);
+              const double fin = dispatch<MS, !Q>(R, srv, svc_of_key_t<SVC>(svc, s0 >> kCntBits), cnt);
               if (Q) {
-                q.P[b * 32] = fin;
+                q.F[s_bid[b * 32 + lane]] = fin;
                 const double lo = __dsub_rn(fin, R.t), hi = __dsub_rn(fin, s_osum[b * 32 + lane]);
-                q.lmin = lo < q.lmin ? lo : q.lmin;
-                q.lmax = hi > q.lmax ? hi : q.lmax;
+                if (lo < q.lm[0]) q.lm[0] = lo;
+                if (hi > q.lm[32]) q.lm[32] = hi;
               }
             } else {
               leftover += s_osum[b * 32 + lane];
-              if (Q) q.P[b * 32] = BB_QNAN;  // never completes
+              if (Q) q.F[s_bid[b * 32 + lane]] = BB_QNAN;  // never completes
             }
           }
         }
@@ -472,6 +478,10 @@ __global__ void __launch_bounds__(kGenThreads, Q ? 2 : BB_GEN_MINB) gen_kernel(c
           lat_out = (R.latw - (R.asum - leftover)) / (double)R.ncomp;
           q_ok = Q;
           q_m = R.ncomp;
+          if (Q) {
+            q_lmin = q.lm[0];
+            q_lmax = q.lm[32];
+          }
         } else {
           mk_out = thr_out = busy_out = lat_out = failed ? BB_QNAN : 0.0;
         }
@@ -595,8 +605,8 @@ __global__ void __launch_bounds__(kGenThreads, Q ? 2 : BB_GEN_MINB) gen_kernel(c
               const double fin = dispatch<true>(R, srv, ovS[(size_t)x * gstride], ovM[(size_t)x * gstride]);
               if (Q) {  // the batch list now holds completions
                 ovS[(size_t)x * gstride] = fin;
-                q.lmin = fmin(q.lmin, fin);
-                q.lmax = fmax(q.lmax, fin);
+                q_lmin = fmin(q_lmin, fin);
+                q_lmax = fmax(q_lmax, fin);
               }
             }
             busy = R.busy;
@@ -607,8 +617,8 @@ __global__ void __launch_bounds__(kGenThreads, Q ? 2 : BB_GEN_MINB) gen_kernel(c
             for (uint32_t x = 0; x < nbt; ++x) {
               D = __dadd_rn(D, ovS[(size_t)x * gstride]);
               ovS[(size_t)x * gstride] = D;
-              q.lmin = fmin(q.lmin, D);
-              q.lmax = fmax(q.lmax, D);
+              q_lmin = fmin(q_lmin, D);
+              q_lmax = fmax(q_lmax, D);
             }
           }
           if (nc > 0) {
@@ -635,24 +645,25 @@ __global__ void __launch_bounds__(kGenThreads, Q ? 2 : BB_GEN_MINB) gen_kernel(c
         const uint32_t l = __ffs(pend) - 1;
         pend &= pend - 1;
         const uint64_t m = __shfl_sync(kQFull, q_m, l);
-        const double lmin = __shfl_sync(kQFull, q.lmin, l), lmax = __shfl_sync(kQFull, q.lmax, l);
+        const double lmin = __shfl_sync(kQFull, q_lmin, l), lmax = __shfl_sync(kQFull, q_lmax, l);
         const size_t ls = (size_t)blockIdx.x * kGenThreads + wib * 32 + l;
         double v50, v99;
         if (!OVL) {
-          const uint32_t ncl = __shfl_sync(kQFull, q.nc, l);
-          double* A_l = L.qA + qwarp * L.q_n * 32 + l * 32;
-          QSrcLogRev first{A_l, L.qB + qwarp * L.q_n * 32 + l * 32, L.qF + qwarp * L.q_nf * 32 + l,
-                           L.qP + qwarp * kmax * 32 + l, q_carry, n, ncl, k, lane, 0.0};
+          double* A_l = L.qA + qwarp * L.q_n * 32 + l * kQRun;
+          double sum = 0.0;  // latency_mean from the latencies themselves
+#if BB_QWRITE
+          QSrcLog<true> first{A_l, L.qI + qwarp * L.q_n * 32 + l * kQRun, L.qF + ls * L.q_nf, n, lane};
           const QSrcLat rest{A_l, n, lane};
-          q_select(first, rest, m, lmin, lmax, wreg, qregion, q_ans, lane, v50, v99);
-          double sum = first.sum;  // latency_mean from the latencies themselves
-#pragma unroll
-          for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(kQFull, sum, o);
+          q_select(first, rest, m, lmin, lmax, wreg, qregion, q_ans, lane, v50, v99, &sum);
+#else
+          const QSrcLog<false> src{A_l, L.qI + qwarp * L.q_n * 32 + l * kQRun, L.qF + ls * L.q_nf, n, lane};
+          q_select(src, src, m, lmin, lmax, wreg, qregion, q_ans, lane, v50, v99, &sum);
+#endif
           if (lane == l) lat_out = sum / (double)m;
         } else {
           const uint32_t nb = __shfl_sync(kQFull, q_nb, l);
           QSrcBatches src{L.ovS + ls, L.ovM + ls, gstride, nb, lane};
-          q_select(src, src, m, lmin, lmax, wreg, qregion, q_ans, lane, v50, v99);
+          q_select(src, src, m, lmin, lmax, wreg, qregion, q_ans, lane, v50, v99, nullptr);
         }
         if (lane == l) {
           q_p50 = v50;
@@ -701,7 +712,7 @@ cudaError_t launch_gen(const GenLaunch& L, cudaStream_t s) {
   const bool blist = OVL && (MS || Q), rlog = Q && !OVL;
   const uint64_t q_n = rlog ? ((uint64_t)L.n_max + 31) & ~31ull : 0, q_nf = rlog ? L.nf_max : 0;
   const uint64_t per_thread = (blist ? (uint64_t)L.nb_max * (sizeof(double) + sizeof(uint16_t)) : 0) +
-                              (rlog ? q_n * 9 + (q_nf + L.k_max) * sizeof(double) : 0);
+                              (rlog ? q_n * 12 + q_nf * sizeof(double) : 0);
   bool held = false;
   if (per_thread) {
     // quantile mode may use most of HBM (a 10^5-request log is 0.9 MB per
@@ -712,7 +723,7 @@ cudaError_t launch_gen(const GenLaunch& L, cudaStream_t s) {
     grid = (unsigned)(grid < max_grid ? grid : max_grid);
     const uint64_t slots = (uint64_t)grid * kGenThreads;
     const uint64_t nbl = blist ? slots * L.nb_max : 0;
-    const uint64_t bytes = nbl * (sizeof(double) + sizeof(uint16_t)) + slots * (q_n * 9 + (q_nf + L.k_max) * 8) + 1024;
+    const uint64_t bytes = nbl * (sizeof(double) + sizeof(uint16_t)) + slots * (q_n * 12 + q_nf * 8) + 1024;
     unsigned char* base = nullptr;
     e = gen_scratch_acquire(bytes, s, reinterpret_cast<void**>(&base));
     if (e != cudaSuccess) return e;
@@ -728,10 +739,9 @@ cudaError_t launch_gen(const GenLaunch& L, cudaStream_t s) {
     if (rlog) {
       L2.qA = reinterpret_cast<double*>(carve(slots * q_n * sizeof(double)));
       L2.qF = reinterpret_cast<double*>(carve(slots * q_nf * sizeof(double)));
-      L2.qP = reinterpret_cast<double*>(carve(slots * L.k_max * sizeof(double)));
+      L2.qI = reinterpret_cast<uint32_t*>(carve(slots * q_n * sizeof(uint32_t)));
     }
     if (blist) L2.ovM = reinterpret_cast<uint16_t*>(carve(nbl * sizeof(uint16_t)));
-    if (rlog) L2.qB = reinterpret_cast<uint8_t*>(carve(slots * q_n));
     L2.q_n = q_n;
     L2.q_nf = q_nf;
   }

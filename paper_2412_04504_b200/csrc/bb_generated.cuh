@@ -55,11 +55,10 @@ struct GenLaunch {
   // quantile mode (bb_quantile.cuh): exact per-replication p50/p99
   int32_t quant;
   uint32_t n_max;           // most requests of any point in the launch
-  uint32_t nf_max;          // most full batches of any point (n/B + 1)
-  double* qA;               // request log per resident thread [slot][q_n] (set by gen_run)
-  uint8_t* qB;              //   (bin | closed) bytes [slot][q_n]
-  double* qF;               //   full-batch completions [slot][q_nf]
-  double* qP;               //   per-bin first arrival / partial completion [slot][k_max]
+  uint32_t nf_max;          // most batches of any point (n/B + k + 1)
+  double* qA;               // request log: arrivals (set by gen_run; layout in bb_quantile.cuh)
+  uint32_t* qI;             //   batch ids
+  double* qF;               //   completion per batch id [slot][q_nf]
   uint64_t q_n, q_nf;
 };
 

@@ -967,7 +967,7 @@ void launch_sweep(const SweepParams* E, Sweep& W, uint64_t rep_begin, uint64_t r
         smax = std::max(smax, W.gp[j].n_servers);
         nbmax = std::max<uint64_t>(nbmax, W.gp[j].n / W.gp[j].B + W.gp[j].k + 1);
         nmax = std::max(nmax, W.gp[j].n);
-        nfmax = std::max(nfmax, W.gp[j].n / W.gp[j].B + 1);
+        nfmax = std::max(nfmax, W.gp[j].n / W.gp[j].B + W.gp[j].k + 1);
       }
     const bb::GenPoint* base = W.d_pts.as<bb::GenPoint>();
     DBuf grp;

@@ -51,35 +51,94 @@ __device__ __forceinline__ uint64_t qwidth(uint32_t sh) { return sh >= 64 ? ~0ul
 // that many independent HBM loads in flight (the pass is latency bound
 // otherwise).
 constexpr int kQGroup = 8;
-constexpr int kQChunk = 16;  // latency source: tiles per pipelined step
+#ifndef BB_QCHUNK
+#define BB_QCHUNK 8
+#endif
+constexpr int kQChunk = BB_QCHUNK;  // request-log sources: runs per pipelined step
 
-// Request-log layout (finite rate).  A warp's 32 replications share rows
-// interleaved in blocks of 32 requests: request i of lane l lives at
-// [(i/32)*1024 + l*32 + i%32] (arrivals, then latencies, fp64; the bytes
-// alike).  The lanes walk their requests in lockstep, so a warp's stores and
-// loads of one block stay inside 8 KB (full sectors once L2 merges them),
-// and one replication's 32-request run is a contiguous 256 B that a warp
-// reads in one coalesced access.  Completions of full batches: [c*32 + l].
-// Rows are padded to a multiple of 32 requests.
+// Request-log layout (finite rate).  Every batch gets an id when its first
+// member arrives (its bin's open batch; ids count openings per replication),
+// and every request logs (arrival, batch id); a batch's completion is written
+// once, at its id, when it is dispatched (drained partials at the end; NaN if
+// it never completes).  So latency_i = F[id_i] - a_i -- the reference's
+// subtraction (simulator.hpp:293) -- for every request independently.
+//
+// A warp's 32 replications share rows interleaved in runs of kQRun
+// requests: request i of lane l lives at [(i/R)*32R + l*R + i%R] (arrival
+// fp64, id u32).  The lanes walk their requests in lockstep, so one store
+// instruction of the forward pass covers 32 runs side by side (few cache
+// lines), and the selection's warp-wide reads of one replication cover
+// 32/R runs.  Completions: a contiguous row per lane.  Rows are padded to a
+// multiple of 32 requests.
+#ifndef BB_QRUN
+#define BB_QRUN 32
+#endif
+constexpr uint32_t kQRun = BB_QRUN;
+__host__ __device__ __forceinline__ size_t qlog_index(uint32_t i) {
+  return (size_t)(i / kQRun) * (32 * kQRun) + (i % kQRun);
+}
 
-// Finite arrival rate: one replication's latencies (NaN: never completed, or
-// padding), converted in place from the request log by q_log_to_latency.
-// L points at the replication's first run (stride 1024 doubles per run).
+template <bool WRITE>
+struct QSrcLog {
+  double* A;            // the replication's first run (+ qlog_index(i))
+  const uint32_t* Id;   //   its batch ids, same layout
+  const double* F;      // its completions by batch id
+  uint32_t n, lane;
+
+  template <class Fn>
+  __device__ void for_each(Fn&& f) const {
+    // kQChunk runs per step; the next step's loads are issued before this
+    // step's values are used
+    const uint32_t nt = (n + 31) / 32;
+    double na[kQChunk];
+    uint32_t nid[kQChunk];
+    auto load = [&](uint32_t t0) {
+#pragma unroll
+      for (int u = 0; u < kQChunk; ++u) {
+        const uint32_t t = t0 + u;
+        const bool v = t < nt && t * 32 + lane < n;
+        const size_t o = qlog_index(t * 32 + lane);
+        na[u] = v ? A[o] : 0.0;
+        nid[u] = v ? Id[o] : 0xFFFFFFFFu;
+      }
+    };
+    load(0);
+    for (uint32_t t0 = 0; t0 < nt; t0 += kQChunk) {
+      double a[kQChunk], fin[kQChunk];
+      uint32_t id[kQChunk];
+#pragma unroll
+      for (int u = 0; u < kQChunk; ++u) {
+        a[u] = na[u];
+        id[u] = nid[u];
+      }
+      if (t0 + kQChunk < nt) load(t0 + kQChunk);
+#pragma unroll
+      for (int u = 0; u < kQChunk; ++u) fin[u] = id[u] != 0xFFFFFFFFu ? F[id[u]] : BB_QNAN;
+#pragma unroll
+      for (int u = 0; u < kQChunk; ++u) {
+        const double x = __dsub_rn(fin[u], a[u]);
+        const uint32_t t = t0 + u;
+        if (WRITE && t < nt) A[qlog_index(t * 32 + lane)] = x;  // later passes read QSrcLat
+        f(x, isnan(x) ? 0u : 1u);
+      }
+    }
+  }
+};
+
+// Later passes: the latencies the first pass wrote over the arrivals.
 struct QSrcLat {
   const double* L;
   uint32_t n, lane;
 
   template <class Fn>
   __device__ void for_each(Fn&& f) const {
-    // kQChunk tiles per step; the next step's loads are issued before this
-    // step's values are used
     const uint32_t nt = (n + 31) / 32;
     double nx[kQChunk];
     auto load = [&](uint32_t t0) {
 #pragma unroll
       for (int u = 0; u < kQChunk; ++u) {
         const uint32_t t = t0 + u;
-        nx[u] = (t < nt && t * 32 + lane < n) ? L[(size_t)t * 1024 + lane] : BB_QNAN;
+        nx[u] = (t < nt && t * 32 + lane < n) ? L[qlog_index(t * 32 + lane)] : BB_QNAN;
       }
     };
     load(0);
@@ -90,75 +149,6 @@ struct QSrcLat {
       if (t0 + kQChunk < nt) load(t0 + kQChunk);
 #pragma unroll
       for (int u = 0; u < kQChunk; ++u) f(x[u], isnan(x[u]) ? 0u : 1u);
-    }
-  }
-};
-
-// Finite arrival rate, first pass: one replication's request log read
-// newest tile first.  A request belongs to the batch closed by the next
-// closing request of its bin (or to its bin's drained partial), so
-// __match_any_sync over the bins and a ballot of the closing flags give each
-// lane the completion of its batch; a per-bin carry crosses tiles.  latency =
-// completion - arrival (the reference's subtraction, simulator.hpp:293) is
-// written over the arrival, so later passes read QSrcLat, and summed per lane
-// (latency_mean).  kQGroup tiles are loaded, then their completions gathered,
-// before any carry is resolved.
-struct QSrcLogRev {
-  double* A;            // the replication's first run (stride 1024 per run)
-  const uint8_t* Bf;    //   its bytes, same layout
-  const double* F;      // completions: F[c*32] for closing c
-  const double* P;      // per bin: P[b*32] completion of the drained partial (NaN: none)
-  double* carry;        // shared, per bin
-  uint32_t n, nclose, k, lane;
-  double sum;           // this lane's share of the latency sum
-
-  template <class Fn>
-  __device__ void for_each(Fn&& f) {
-    for (uint32_t b = lane; b < k; b += 32) carry[b] = P[b * 32];
-    __syncwarp();
-    const uint32_t lt = (1u << lane) - 1u;
-    uint32_t cend = nclose;
-    for (int32_t thi = (int32_t)((n + 31) / 32); thi > 0; thi -= kQGroup) {
-      double a[kQGroup], fin[kQGroup];
-      uint32_t byte[kQGroup], peers[kQGroup], cm[kQGroup];
-      int32_t fi[kQGroup];
-#pragma unroll
-      for (int u = 0; u < kQGroup; ++u) {  // tile thi-1-u, all loads issued together
-        const int32_t t = thi - 1 - u;
-        const bool valid = t >= 0 && (uint32_t)t * 32u + lane < n;
-        a[u] = valid ? A[(size_t)t * 1024 + lane] : 0.0;
-        byte[u] = valid ? (uint32_t)Bf[(size_t)t * 1024 + lane] : kQBinInvalid;
-      }
-#pragma unroll
-      for (int u = 0; u < kQGroup; ++u) {
-        const uint32_t b = byte[u] & 0x7F, c = byte[u] >> 7;
-        peers[u] = __match_any_sync(kQFull, b);
-        cm[u] = __ballot_sync(kQFull, c);
-        const uint32_t cbase = cend - __popc(cm[u]);
-        const uint32_t cand = peers[u] & cm[u] & ~lt;  // closings of my bin at or after me
-        fi[u] = cand ? (int32_t)(cbase + __popc(cm[u] & ((1u << (__ffs(cand) - 1)) - 1u))) : -1;
-        cend = cbase;
-      }
-#pragma unroll
-      for (int u = 0; u < kQGroup; ++u) fin[u] = fi[u] >= 0 ? F[(size_t)fi[u] * 32] : BB_QNAN;
-#pragma unroll
-      for (int u = 0; u < kQGroup; ++u) {  // per-bin carry, newest tile first
-        const uint32_t b = byte[u] & 0x7F, c = byte[u] >> 7;
-        if (fi[u] < 0 && b != kQBinInvalid) fin[u] = carry[b];
-        __syncwarp();
-        if (c && !(peers[u] & cm[u] & lt)) carry[b] = fin[u];  // earliest closing of its bin
-        __syncwarp();
-      }
-#pragma unroll
-      for (int u = 0; u < kQGroup; ++u) {
-        const int32_t t = thi - 1 - u;
-        const bool valid = byte[u] != kQBinInvalid;
-        const double x = valid ? __dsub_rn(fin[u], a[u]) : BB_QNAN;
-        if (t >= 0) A[(size_t)t * 1024 + lane] = x;  // padding lanes become NaN
-        const bool ok = !isnan(x);
-        if (ok) sum += x;
-        f(x, ok ? 1u : 0u);
-      }
     }
   }
 };
@@ -195,7 +185,7 @@ struct QSrcBatches {
 template <class Src1, class Src>
 __device__ void q_select(Src1& first, const Src& src, uint64_t m, double lmin, double lmax, unsigned char* region,
                          uint32_t region_bytes, double* ans, uint32_t lane, double& p50,
-                         double& p99) {
+                         double& p99, double* wsum) {
   uint32_t* hist = reinterpret_cast<uint32_t*>(region);
   const uint32_t cap = ((region_bytes - 1024u) / 10u) & ~7u;  // + a 256-bucket histogram
   double* cx = reinterpret_cast<double*>(region);
@@ -225,18 +215,26 @@ __device__ void q_select(Src1& first, const Src& src, uint64_t m, double lmin, d
 
   // one histogram pass over the range (glo, gsh); every target in that range
   // moves to the sub-bucket holding its rank
-  auto refine = [&](auto& source, uint64_t glo, uint32_t gsh) {
+  // (the first pass also sums the values for the caller, when asked)
+  auto refine = [&](auto& source, uint64_t glo, uint32_t gsh, bool sum) {
     const uint32_t s2 = gsh >= 64 ? sh0 : (gsh > 11 ? gsh - 11 : 0);
     for (uint32_t j = lane; j < kQBuckets; j += 32) hist[j] = 0;
     __syncwarp();
     const uint64_t gw = qwidth(gsh);
+    double acc = 0.0;
     source.for_each([&](double x, uint32_t w) {
+      if (sum && w) acc += x * (double)w;
       const uint64_t d = qkey(x) - glo;
       if (w && d < gw) {
         const uint64_t bk = d >> s2;
         atomicAdd(&hist[bk < kQBuckets ? bk : kQBuckets - 1], w);
       }
     });
+    if (sum) {
+#pragma unroll
+      for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(kQFull, acc, o);
+      *wsum = acc;
+    }
     __syncwarp();
     uint32_t loc = 0;
     for (uint32_t j = 0; j < kQBuckets / 32; ++j) loc += hist[lane * (kQBuckets / 32) + j];
@@ -276,7 +274,7 @@ __device__ void q_select(Src1& first, const Src& src, uint64_t m, double lmin, d
     __syncwarp();
   };
 
-  refine(first, kbase, 64);
+  refine(first, kbase, 64, wsum != nullptr);
   for (int iter = 0; iter < 64; ++iter) {
     // a range of one bit pattern holds equal values: resolved without a pass
     uint64_t total = 0;
@@ -304,7 +302,7 @@ __device__ void q_select(Src1& first, const Src& src, uint64_t m, double lmin, d
 #pragma unroll
     for (int t = 0; t < 4; ++t)
       if (t == big) glo = klo[t], gsh = sh[t];
-    refine(src, glo, gsh);
+    refine(src, glo, gsh, false);
   }
 
   bool open = false;

@@ -88,6 +88,9 @@ def full(path, out, requests=None):
         if requests:
             inst = float(row[hdr.index("smsp__inst_executed.sum")].replace(",", ""))
             d["warp_instructions_per_request_step"] = inst * 32 / float(requests)
+            if "dram_bytes_per_launch" in d:
+                d["dram_bytes_per_request"] = d["dram_bytes_per_launch"] / float(requests)
+            d["requests_per_launch"] = float(requests)
         res.append(d)
     json.dump(res if len(res) > 1 else res[0], open(out, "w"), indent=1)
     print(json.dumps(res, indent=1)[:3000])
