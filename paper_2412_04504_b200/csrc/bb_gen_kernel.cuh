@@ -145,7 +145,8 @@ struct QLog {
 };
 
 // One request folded into its bin; closes the batch at B members
-// (on_arrival + form_batch, simulator.hpp:187-254).  Returns 1 when it closed.
+// (on_arrival + form_batch, simulator.hpp:187-254).  Returns the bin's new
+// member count (0: it closed).
 // Quantile mode: osum holds the bin's previous closing time, bid its open
 // batch's id; *id receives the request's batch id.
 template <int SVC, bool track, bool MS, bool Q>
@@ -171,11 +172,11 @@ __device__ __forceinline__ uint32_t fold(Rep& R, uint64_t* __restrict__ slot, do
       if (hi > q.lm[32]) q.lm[32] = hi;  // bounds the first member's (it arrived later)
       *osum = R.t;
     }
-    return 1u;
+    return 0u;
   }
   *slot = km | cnt;
   if (track) *osum += R.t;
-  return 0u;
+  return cnt;
 }
 
 #ifndef BB_QWRITE
@@ -197,16 +198,23 @@ __device__ __forceinline__ uint32_t fold(Rep& R, uint64_t* __restrict__ slot, do
 // (quantile mode, finite rate: the second row set holds each bin's previous
 // closing time instead of the open arrival sums, a third (u32) its open
 // batch's id)
-__host__ __device__ __forceinline__ uint32_t gen_state_bytes(uint32_t kmax, bool ovl, bool track, bool q) {
+// (max_batch_wait: finite rate, a row with each bin's front arrival; overload,
+// two u32 rows with each bin's first arrival and last round-robin formation)
+__host__ __device__ __forceinline__ uint32_t gen_core_bytes(uint32_t kmax, bool ovl, bool track, bool q) {
   if (ovl) return kmax * 768u;
   return q ? kmax * 640u + 512u : kmax * 256u * (track ? 2u : 1u);
 }
-__host__ __device__ __forceinline__ uint32_t gen_warp_bytes(uint32_t kmax, bool ovl, bool track, bool q) {
-  const uint32_t st = gen_state_bytes(kmax, ovl, track, q);
+__host__ __device__ __forceinline__ uint32_t gen_state_bytes(uint32_t kmax, bool ovl, bool track, bool q,
+                                                            bool tm = false) {
+  return gen_core_bytes(kmax, ovl, track, q) + (tm ? kmax * 256u : 0u);
+}
+__host__ __device__ __forceinline__ uint32_t gen_warp_bytes(uint32_t kmax, bool ovl, bool track, bool q,
+                                                           bool tm = false) {
+  const uint32_t st = gen_state_bytes(kmax, ovl, track, q, tm);
   return q ? (st > kQRegionMin ? st : kQRegionMin) + 32u : st;
 }
 
-template <int SVC, int ERR, bool OVL, bool TRACK, bool MS, bool Q>
+template <int SVC, int ERR, bool OVL, bool TRACK, bool MS, bool Q, bool TM>
 __global__ void __launch_bounds__(kGenThreads, Q ? 2 : BB_GEN_MINB) gen_kernel(const __grid_constant__ GenLaunch L) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ uint64_t s_thr[kGenWarps][BB_MAX_BINS + 1];
@@ -219,7 +227,7 @@ __global__ void __launch_bounds__(kGenThreads, Q ? 2 : BB_GEN_MINB) gen_kernel(c
   // per-warp shared region: state rows of 32 lanes ([kmax] packed (key<<11 | cnt),
   // then open arrival sums (finite, no flush) or four u32 tables (overload));
   // in quantile mode the same region then holds the selection histogram
-  const uint32_t wbytes = gen_warp_bytes(kmax, OVL, TRACK, Q);
+  const uint32_t wbytes = gen_warp_bytes(kmax, OVL, TRACK, Q, TM);
   unsigned char* wreg = smem_raw + (size_t)wib * wbytes;
   uint64_t* st = reinterpret_cast<uint64_t*>(wreg);
   double* s_osum = reinterpret_cast<double*>(st + (size_t)kmax * 32);  // finite, no flush
@@ -228,8 +236,13 @@ __global__ void __launch_bounds__(kGenThreads, Q ? 2 : BB_GEN_MINB) gen_kernel(c
   uint32_t* s_cf = s_rem + (size_t)kmax * 32;
   uint32_t* s_jd = s_cf + (size_t)kmax * 32;
   uint32_t* s_bid = reinterpret_cast<uint32_t*>(st + (size_t)kmax * 64);  // quantile mode
-  const uint32_t qregion = gen_state_bytes(kmax, OVL, TRACK, Q) > kQRegionMin
-                               ? gen_state_bytes(kmax, OVL, TRACK, Q) : kQRegionMin;
+  // max_batch_wait: finite rate, each bin's front arrival; overload, each
+  // bin's first arrival and last round-robin formation
+  double* s_front = reinterpret_cast<double*>(wreg + gen_core_bytes(kmax, OVL, TRACK, Q));
+  uint32_t* s_fa = reinterpret_cast<uint32_t*>(s_front);
+  uint32_t* s_li = s_fa + (size_t)kmax * 32;
+  const uint32_t qregion = gen_state_bytes(kmax, OVL, TRACK, Q, TM) > kQRegionMin
+                               ? gen_state_bytes(kmax, OVL, TRACK, Q, TM) : kQRegionMin;
   double* q_ans = reinterpret_cast<double*>(wreg + qregion);  // [4]
 
   const uint32_t nrep = L.rep_end - L.rep_begin;
@@ -334,6 +347,45 @@ __global__ void __launch_bounds__(kGenThreads, Q ? 2 : BB_GEN_MINB) gen_kernel(c
         }
         uint32_t cyc0 = 0;
         const double a0 = __dmul_rn(exp1_tab(draw<SVC>(cyc_rank, nt, 0, c2, c3, cyc0).xg, s_logtab), inv_lambda);
+        // max_batch_wait (simulator.hpp:200-201,223-235): a bin's batch also
+        // forms when its front request has waited W.  With no arrival ties a
+        // bin never holds more than B, so the bin empties at every formation
+        // and its timer is the one armed by its front's arrival.  next_due is
+        // a lower bound on the earliest pending due time (stale dues of bins
+        // that filled up are skipped by the rescan).
+        const double W = TM ? P.max_batch_wait : 0.0;
+        double next_due = CUDART_INF;
+        auto fire_until = [&](double t) {  // on_flush_timer for every due < t, in due order
+          while (next_due < t) {
+            double best = CUDART_INF;
+            uint32_t bb = 0;
+            for (uint32_t b = 0; b < k; ++b)
+              if (st[b * 32 + lane] & kCntMask) {
+                const double due = __dadd_rn(s_front[b * 32 + lane], W);
+                if (due < best) {
+                  best = due;
+                  bb = b;
+                }
+              }
+            next_due = best;
+            if (!(best < t)) break;
+            const uint64_t s0 = st[bb * 32 + lane];
+            const double tn = R.t;
+            R.t = best;  // the batch forms (and joins the FIFO) at the timer's time
+            const double fin = dispatch<MS, !Q>(R, srv, svc_of_key_t<SVC>(svc, s0 >> kCntBits),
+                                                (uint32_t)(s0 & kCntMask));
+            R.t = tn;
+            st[bb * 32 + lane] = 0;
+            if (track) s_osum[bb * 32 + lane] = 0.0;
+            if (Q) {
+              q.F[s_bid[bb * 32 + lane]] = fin;
+              const double lo = __dsub_rn(fin, best), hi = __dsub_rn(fin, s_osum[bb * 32 + lane]);
+              if (lo < q.lm[0]) q.lm[0] = lo;
+              if (hi > q.lm[32]) q.lm[32] = hi;
+              s_osum[bb * 32 + lane] = best;
+            }
+          }
+        };
         // U requests per iteration: their draws, exponentials and bins are
         // independent, so the latencies overlap; the folds stay in order
         constexpr int U = BB_GEN_UNROLL;
@@ -404,10 +456,17 @@ __global__ void __launch_bounds__(kGenThreads, Q ? 2 : BB_GEN_MINB) gen_kernel(c
 #pragma unroll
             for (int u = 0; u < U; ++u) {
               R.t = __dadd_rn(R.t, g[u]);  // exponential inter-arrival, simulator.hpp:181 (no contraction)
+              if (TM) fire_until(R.t);
               if (!Q) R.asum += R.t;
               at[u] = R.t;
-              fold<SVC, TRACK, MS, Q>(R, st + (pb[u] - 1) * 32 + lane, s_osum + (pb[u] - 1) * 32 + lane,
-                                      s_bid + (pb[u] - 1) * 32 + lane, d[u].xs, B, svc, srv, q, qid[u]);
+              const uint32_t c1 = fold<SVC, TRACK, MS, Q>(
+                  R, st + (pb[u] - 1) * 32 + lane, s_osum + (pb[u] - 1) * 32 + lane,
+                  s_bid + (pb[u] - 1) * 32 + lane, d[u].xs, B, svc, srv, q, qid[u]);
+              if (TM && c1 == 1) {  // the bin's front: arm its timer
+                s_front[(pb[u] - 1) * 32 + lane] = R.t;
+                const double due = __dadd_rn(R.t, W);
+                next_due = due < next_due ? due : next_due;
+              }
             }
             if (Q) {  // request log: arrivals and batch ids (16 B stores)
               const size_t o = qlog_index(i);  // (i % 4 == 0: 4 requests stay in one run)
@@ -441,10 +500,16 @@ __global__ void __launch_bounds__(kGenThreads, Q ? 2 : BB_GEN_MINB) gen_kernel(c
           } else {
             const uint32_t p0 = bin_pred(d0.xs, e0);
             R.t = __dadd_rn(R.t, __dmul_rn(exp1_tab(d0.xg, s_logtab), inv_lambda));
+            if (TM) fire_until(R.t);
             if (!Q) R.asum += R.t;
             uint32_t id0 = 0;
-            fold<SVC, TRACK, MS, Q>(R, st + (p0 - 1) * 32 + lane, s_osum + (p0 - 1) * 32 + lane,
+            const uint32_t c1 = fold<SVC, TRACK, MS, Q>(R, st + (p0 - 1) * 32 + lane, s_osum + (p0 - 1) * 32 + lane,
                                     s_bid + (p0 - 1) * 32 + lane, d0.xs, B, svc, srv, q, id0);
+            if (TM && c1 == 1) {
+              s_front[(p0 - 1) * 32 + lane] = R.t;
+              const double due = __dadd_rn(R.t, W);
+              next_due = due < next_due ? due : next_due;
+            }
             if (Q) {
               q.A[qlog_index(i)] = R.t;
               q.Id[qlog_index(i)] = id0;
@@ -452,6 +517,8 @@ __global__ void __launch_bounds__(kGenThreads, Q ? 2 : BB_GEN_MINB) gen_kernel(c
           }
         }
         double leftover = 0.0;
+        // without flush the open batches still form when their timers fire
+        if (TM && !failed && !flush) fire_until(CUDART_INF);
         if (!failed) {
           for (uint32_t b = 0; b < k; ++b) {
             const uint64_t s0 = st[b * 32 + lane];
@@ -503,6 +570,7 @@ __global__ void __launch_bounds__(kGenThreads, Q ? 2 : BB_GEN_MINB) gen_kernel(c
           const uint32_t pb = bin_pred(d.xs, (i & 1u) ? e1 : e0);
           const uint32_t cnt = ++s_F[(pb - 1) * 32 + lane];
           if (cnt == B) s_cf[(pb - 1) * 32 + lane] = i;
+          if (TM && cnt == 1) s_fa[(pb - 1) * 32 + lane] = i;  // arms the bin's first timer
         }
         if (!failed) {
           uint32_t Z = 0;
@@ -516,12 +584,16 @@ __global__ void __launch_bounds__(kGenThreads, Q ? 2 : BB_GEN_MINB) gen_kernel(c
             Z += F >= 1;
             nc += (uint64_t)F * B + (flush ? rem : 0);
           }
+          // max_batch_wait without flush: the partial batches form when their
+          // timers fire at W, after every t = 0 formation (below)
+          const bool timers = TM && !flush && P.max_batch_wait > 0.0;
           cyc = 0;
           double busy = 0.0, latw = 0.0;
           // S > 1 servers: pass 2 files each batch (service, members) under its
           // dispatch index, then the Kiefer-Wolfowitz recursion runs in order
           double* ovS = (MS || Q) ? L.ovS + qslot : nullptr;
           uint16_t* ovM = (MS || Q) ? L.ovM + qslot : nullptr;
+          const uint64_t nc0 = nc;  // requests in batches formed at t = 0
           for (uint32_t i = 0; i < n; ++i) {  // pass 2: same draws, batch positions
             const Draw d = draw<SVC>(cyc_rank, nt, i, c2, c3, cyc);
             if ((i & 1u) == 0) err_pair(i, e0, e1);
@@ -558,13 +630,14 @@ __global__ void __launch_bounds__(kGenThreads, Q ? 2 : BB_GEN_MINB) gen_kernel(c
                 idx = (uint32_t)pos;
               }
               const double S = svc_of_key_t<SVC>(svc, km >> kCntBits);
+              if (TM && j + 1 == s_F[b * 32 + lane]) s_li[b * 32 + lane] = idx;  // rearm_timer's seq
               if (MS || Q) {
                 ovS[idx * gstride] = S;
                 ovM[idx * gstride] = (uint16_t)B;
               }
               if (!MS) {
                 busy += S;
-                latw += S * (double)(nc - before);
+                latw += S * (double)(nc0 - before);
               }
             } else {
               *slot = km | cnt;
@@ -596,12 +669,51 @@ __global__ void __launch_bounds__(kGenThreads, Q ? 2 : BB_GEN_MINB) gen_kernel(c
             }
           }
           double mk = busy;  // one server: all requests arrive at t=0, the server never idles
-          if (MS) {  // S servers: FIFO dispatch over the batches in order (R = 0)
+          const uint32_t nb0 = nbt;  // batches formed at t = 0
+          if (timers) {
+            // fire order at W (simulator.hpp:223-235): the timers armed at the
+            // bins' first arrivals (bins that never filled a batch), then the
+            // ones re-armed by each bin's last round-robin formation
+            const double Wt = P.max_batch_wait;
+            const uint32_t done_bit = 0x80000000u;
+            for (;;) {
+              uint32_t bb = 0xFFFFFFFFu;
+              uint64_t best = ~0ull;
+              for (uint32_t b = 0; b < k; ++b) {
+                const uint32_t rem = s_rem[b * 32 + lane];
+                if (!rem || (rem & done_bit)) continue;
+                const uint32_t F = s_F[b * 32 + lane];
+                const uint64_t key = F ? (uint64_t)n + s_li[b * 32 + lane] : s_fa[b * 32 + lane];
+                if (key < best) {
+                  best = key;
+                  bb = b;
+                }
+              }
+              if (bb == 0xFFFFFFFFu) break;
+              const uint32_t rem = s_rem[bb * 32 + lane];
+              s_rem[bb * 32 + lane] = rem | done_bit;
+              const double S = svc_of_key_t<SVC>(svc, st[bb * 32 + lane] >> kCntBits);
+              nc += rem;
+              if (MS || Q) {
+                ovS[(size_t)nbt * gstride] = S;
+                ovM[(size_t)nbt * gstride] = (uint16_t)rem;
+              }
+              if (!MS) {  // one server: D = max(D, W) + S
+                mk = __dadd_rn(fmax(mk, Wt), S);
+                busy += S;
+                latw += (double)rem * mk;
+              }
+              ++nbt;
+            }
+            for (uint32_t b = 0; b < k; ++b) s_rem[b * 32 + lane] &= ~done_bit;
+          }
+          if (MS) {  // S servers: FIFO dispatch over the batches in order (R = 0, or W for timers)
             Rep R{0.0, 0.0, 0.0, 0.0, 0.0, 0};
             Servers srv{P.n_servers ? P.n_servers : 1u, L.srv + (size_t)blockIdx.x * blockDim.x + tid,
                         (uint32_t)gstride};
             for (uint32_t q = 0; q < srv.S; ++q) srv.V[(size_t)q * srv.stride] = 0.0;
             for (uint32_t x = 0; x < nbt; ++x) {
+              R.t = x < nb0 ? 0.0 : P.max_batch_wait;
               const double fin = dispatch<true>(R, srv, ovS[(size_t)x * gstride], ovM[(size_t)x * gstride]);
               if (Q) {  // the batch list now holds completions
                 ovS[(size_t)x * gstride] = fin;
@@ -615,7 +727,7 @@ __global__ void __launch_bounds__(kGenThreads, Q ? 2 : BB_GEN_MINB) gen_kernel(c
           } else if (Q) {  // one server: completions are the running sum in dispatch order
             double D = 0.0;
             for (uint32_t x = 0; x < nbt; ++x) {
-              D = __dadd_rn(D, ovS[(size_t)x * gstride]);
+              D = __dadd_rn(x < nb0 ? D : fmax(D, P.max_batch_wait), ovS[(size_t)x * gstride]);
               ovS[(size_t)x * gstride] = D;
               q_lmin = fmin(q_lmin, D);
               q_lmax = fmax(q_lmax, D);
@@ -687,10 +799,10 @@ __global__ void __launch_bounds__(kGenThreads, Q ? 2 : BB_GEN_MINB) gen_kernel(c
 
 
 
-template <int SVC, int ERR, bool OVL, bool TRACK, bool MS, bool Q>
+template <int SVC, int ERR, bool OVL, bool TRACK, bool MS, bool Q, bool TM = false>
 cudaError_t launch_gen(const GenLaunch& L, cudaStream_t s) {
-  const size_t smem = (size_t)gen_warp_bytes(L.k_max, OVL, TRACK, Q) * kGenWarps;
-  auto kern = gen_kernel<SVC, ERR, OVL, TRACK, MS, Q>;
+  const size_t smem = (size_t)gen_warp_bytes(L.k_max, OVL, TRACK, Q, TM) * kGenWarps;
+  auto kern = gen_kernel<SVC, ERR, OVL, TRACK, MS, Q, TM>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 0, occ = 0;
@@ -761,18 +873,23 @@ cudaError_t launch_gen(const GenLaunch& L, cudaStream_t s) {
   return e;
 }
 
+template <int SVC, int ERR, bool Q, bool TM>
+cudaError_t launch_mode_qt(const GenLaunch& L, cudaStream_t s) {
+  if (L.overload)
+    return L.s_max > 1 ? launch_gen<SVC, ERR, true, false, true, Q, TM>(L, s)
+                       : launch_gen<SVC, ERR, true, false, false, Q, TM>(L, s);
+  // S > 1 servers: leftover sums kept; quantile mode sums the latencies
+  // themselves (no open arrival sums)
+  if (L.s_max > 1) return launch_gen<SVC, ERR, false, !Q, true, Q, TM>(L, s);
+  if constexpr (!Q) {
+    if (L.track) return launch_gen<SVC, ERR, false, true, false, Q, TM>(L, s);
+  }
+  return launch_gen<SVC, ERR, false, false, false, Q, TM>(L, s);
+}
+
 template <int SVC, int ERR, bool Q>
 cudaError_t launch_mode_q(const GenLaunch& L, cudaStream_t s) {
-  if (L.overload)
-    return L.s_max > 1 ? launch_gen<SVC, ERR, true, false, true, Q>(L, s)
-                       : launch_gen<SVC, ERR, true, false, false, Q>(L, s);
-  // S > 1 servers: finite rates only (validated on the host); leftover sums kept
-  // (quantile mode sums the latencies themselves: no open arrival sums)
-  if (L.s_max > 1) return launch_gen<SVC, ERR, false, !Q, true, Q>(L, s);
-  if constexpr (!Q) {
-    if (L.track) return launch_gen<SVC, ERR, false, true, false, Q>(L, s);
-  }
-  return launch_gen<SVC, ERR, false, false, false, Q>(L, s);
+  return L.timers ? launch_mode_qt<SVC, ERR, Q, true>(L, s) : launch_mode_qt<SVC, ERR, Q, false>(L, s);
 }
 
 template <int SVC, int ERR>

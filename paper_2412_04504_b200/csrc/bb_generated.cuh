@@ -15,6 +15,7 @@ struct GenPoint {
   uint32_t check_domain;    // keys outside [vlo, vhi] raise domain_error
   uint32_t gidx;            // global point index (output row)
   uint32_t n_servers;       // S (simulator.hpp:68)
+  double max_batch_wait;    // W > 0, or 0 (no timers; simulator.hpp:70)
   uint64_t vlo, vhi;
   uint64_t e_t1, e_t2;      // symmetric: u < p <=> x < t1 ; u >= 1-p <=> x >= t2
   const double* edges;      // k+1 (device), input of the threshold setup
@@ -53,6 +54,7 @@ struct GenLaunch {
   uint16_t* ovM;            //   ... and member counts
   DevError* err;
   // quantile mode (bb_quantile.cuh): exact per-replication p50/p99
+  int32_t timers;           // some point has max_batch_wait (the timer kernels)
   int32_t quant;
   uint32_t n_max;           // most requests of any point in the launch
   uint32_t nf_max;          // most batches of any point (n/B + k + 1)

@@ -877,7 +877,10 @@ void build_sweep(std::vector<bb_run_template> tpl, Sweep& W, cudaStream_t st, bo
   for (auto& t : W.tpl) {
     W.spec.push_back(materialize(t, 0));
     const SimSpec& s = W.spec.back();
-    if (t.has_max_batch_wait) raise(BB_EUNSUPPORTED, "max_batch_wait is not implemented on the GPU path yet");
+    if (t.has_max_batch_wait && !generated)
+      raise(BB_EUNSUPPORTED, "max_batch_wait with reference streams is not implemented on the GPU path yet");
+    if (t.has_max_batch_wait && !(t.max_batch_wait > 0))
+      raise(BB_EINVAL, "sim config: max_batch_wait must be positive");  // simulator.hpp:160-161
     if (!generated) continue;
     if (s.S > 4096) raise(BB_EUNSUPPORTED, "more than 4096 servers is not supported");
     if (s.k() > BB_MAX_BINS) raise(BB_EUNSUPPORTED, "more than 64 bins is not supported");
@@ -926,6 +929,7 @@ void build_sweep(std::vector<bb_run_template> tpl, Sweep& W, cudaStream_t st, bo
     g.err_kind = s.error_draws() ? (uint32_t)s.err_kind : 0u;
     g.gidx = (uint32_t)i;
     g.n_servers = (uint32_t)s.S;
+    g.max_batch_wait = W.tpl[i].has_max_batch_wait ? W.tpl[i].max_batch_wait : 0.0;
     if (g.err_kind == 1) {
       g.e_t1 = (uint64_t)std::ceil(s.p * 0x1.0p53);
       g.e_t2 = (uint64_t)std::ceil((1.0 - s.p) * 0x1.0p53);
@@ -944,12 +948,13 @@ void launch_sweep(const SweepParams* E, Sweep& W, uint64_t rep_begin, uint64_t r
   // group points by kernel instantiation; each group's points are copied
   // (already threshold-resolved) into a contiguous device array
   struct Key {
-    int err, cyc, ovl, track, ms;
+    int err, cyc, ovl, track, ms, tm;
   };
   std::vector<Key> keys(P);
   for (size_t i = 0; i < P; ++i)
     keys[i] = Key{(int)W.gp[i].err_kind, (int)W.gp[i].svc.kind, W.gp[i].inv_lambda == 0.0,
-                  W.gp[i].inv_lambda != 0.0 && !W.gp[i].flush, W.gp[i].n_servers > 1};
+                  W.gp[i].inv_lambda != 0.0 && !W.gp[i].flush, W.gp[i].n_servers > 1,
+                  W.gp[i].max_batch_wait > 0.0};
   std::vector<bool> done(P, false);
   bool first = true;
   for (size_t i = 0; i < P; ++i) {
@@ -960,14 +965,16 @@ void launch_sweep(const SweepParams* E, Sweep& W, uint64_t rep_begin, uint64_t r
     for (size_t j = i; j < P; ++j)
       if (!done[j] && keys[j].err == keys[i].err && keys[j].cyc == keys[i].cyc &&
           keys[j].ovl == keys[i].ovl && keys[j].track == keys[i].track &&
-          keys[j].ms == keys[i].ms) {
+          keys[j].ms == keys[i].ms && keys[j].tm == keys[i].tm) {
         members.push_back((uint32_t)j);
         done[j] = true;
         kmax = std::max(kmax, W.gp[j].k);
         smax = std::max(smax, W.gp[j].n_servers);
         nbmax = std::max<uint64_t>(nbmax, W.gp[j].n / W.gp[j].B + W.gp[j].k + 1);
         nmax = std::max(nmax, W.gp[j].n);
-        nfmax = std::max(nfmax, W.gp[j].n / W.gp[j].B + W.gp[j].k + 1);
+        // batch ids per replication: n/B full + k partials, or up to n with timers
+        nfmax = std::max(nfmax, W.gp[j].max_batch_wait > 0.0 ? W.gp[j].n + 1
+                                                             : W.gp[j].n / W.gp[j].B + W.gp[j].k + 1);
       }
     const bb::GenPoint* base = W.d_pts.as<bb::GenPoint>();
     DBuf grp;
@@ -1000,6 +1007,7 @@ void launch_sweep(const SweepParams* E, Sweep& W, uint64_t rep_begin, uint64_t r
     L.overload = keys[i].ovl;
     L.out = rep_dev;
     L.quant = bb::g_gen_quantiles.load() ? 1 : 0;
+    L.timers = keys[i].tm;
     L.n_max = nmax;
     L.nf_max = nfmax;
     DBuf err(sizeof(bb::DevError), st);

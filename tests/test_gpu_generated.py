@@ -7,6 +7,7 @@ import math
 
 import numpy as np
 import pytest
+import torch
 
 import oracle_py as O
 import paper_2412_04504_b200 as bb
@@ -235,3 +236,30 @@ def test_multi_server_overload_vs_reference(S, k, flush):
                          200)
     assert within_3se(p.throughput_mean, p.throughput_std, 2000, thr)
     assert within_3se(p.latency_mean, p.latency_std, 2000, lat)
+
+
+# ------------------------------------------------------------- max_batch_wait
+@pytest.mark.parametrize("W,flush,S", [(4.0, True, 1), (2.0, False, 1), (1.5, True, 8)])
+def test_max_batch_wait_vs_reference(W, flush, S):
+    """Timers (simulator.hpp:200-201,223-235) in the fused kernel: point means
+    (throughput, latency, p50) within 3 SE of the reference's own replications.
+    (Short waits form small batches: the queue can then overload, as in the
+    reference.)"""
+    lam = 0.6 * S
+    base = dict(arrival_rate=lam, n_requests=10_000, batch_size=16, n_servers=S,
+                flush_partial=flush)
+    t = template(bins=bb.BinRule(k=4), max_batch_wait=W, **base)
+    p = bb.run_point(t, 31, 2000)
+    ms, _ = O.run_replicas(dict(base, edges=bb.uniform_boundaries(4, 1.0, 20.0).edges, lo=1.0,
+                                hi=20.0, max_batch_wait=W), 4242, 0, 300, THREADS)
+    thr = np.array([m["throughput"] for m in ms])
+    lat = np.array([m["latency_mean"] for m in ms])
+    assert within_3se(p.throughput_mean, p.throughput_std, 2000, thr)
+    assert within_3se(p.latency_mean, p.latency_std, 2000, lat)
+    p50 = np.array([m["latency_p50"] for m in ms])
+    rep = torch.zeros(6 * 2000, dtype=torch.float64, device="cuda")
+    bb.points_shard_device([t], 2000, 31, 0, 2000, rep.data_ptr())
+    torch.cuda.synchronize()
+    g50 = rep.view(6, 2000)[2].cpu().numpy()
+    assert g50.mean() == pytest.approx(p.latency_p50, rel=1e-12)
+    assert within_3se(g50.mean(), g50.std(ddof=1), 2000, p50)

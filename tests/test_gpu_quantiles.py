@@ -89,25 +89,33 @@ def kernel_rep_metrics(t, reps, master):
 
 
 CASES = [
-    # (lambda, n, B, k, servers, flush, p_error)
-    (0.9, 20000, 8, 4, 1, True, 0.0),
-    (1.3, 30000, 16, 8, 1, True, 0.15),
-    (0.6, 12000, 4, 1, 1, True, 0.0),
-    (1.1, 20000, 16, 4, 1, False, 0.0),      # no flush: open partials never complete
-    (3.0, 20000, 8, 3, 4, True, 0.0),        # Kiefer-Wolfowitz dispatch, 4 servers
-    (math.inf, 9000, 32, 4, 1, True, 0.0),   # overload, drains in bin order
-    (math.inf, 9000, 32, 4, 1, False, 0.1),  # overload, round-robin rounds
-    (math.inf, 6000, 16, 2, 3, True, 0.0),   # overload, 3 servers
-    (5.0, 777, 8, 16, 1, True, 0.0),         # short run, ragged tail
+    # (lambda, n, B, k, servers, flush, p_error, max_batch_wait)
+    (0.9, 20000, 8, 4, 1, True, 0.0, None),
+    (1.3, 30000, 16, 8, 1, True, 0.15, None),
+    (0.6, 12000, 4, 1, 1, True, 0.0, None),
+    (1.1, 20000, 16, 4, 1, False, 0.0, None),      # no flush: open partials never complete
+    (3.0, 20000, 8, 3, 4, True, 0.0, None),        # Kiefer-Wolfowitz dispatch, 4 servers
+    (math.inf, 9000, 32, 4, 1, True, 0.0, None),   # overload, drains in bin order
+    (math.inf, 9000, 32, 4, 1, False, 0.1, None),  # overload, round-robin rounds
+    (math.inf, 6000, 16, 2, 3, True, 0.0, None),   # overload, 3 servers
+    (5.0, 777, 8, 16, 1, True, 0.0, None),         # short run, ragged tail
+    # max_batch_wait (simulator.hpp:200-201,223-235)
+    (0.8, 20000, 16, 4, 1, True, 0.0, 6.0),        # timers and full batches mixed
+    (0.5, 15000, 32, 8, 1, False, 0.1, 3.0),       # no flush: the last partials time out too
+    (2.0, 20000, 16, 4, 8, True, 0.0, 1.5),        # 8 servers (the reference's timer test shape)
+    (0.3, 8000, 8, 1, 1, True, 0.0, 0.5),          # almost every batch formed by its timer
+    (math.inf, 9000, 32, 4, 1, False, 0.0, 2.0),   # overload: partials form at W, in arming order
+    (math.inf, 9003, 32, 5, 2, False, 0.1, 1e6),   # ... with 2 servers, server idle until W
+    (math.inf, 9000, 32, 4, 1, True, 0.0, 2.0),    # overload + flush: the timers go stale
 ]
 
 
 @pytest.mark.parametrize("case", CASES)
 def test_replication_quantiles_bit_exact(case):
-    lam, n, B, k, S, flush, pe = case
+    lam, n, B, k, S, flush, pe, W = case
     lo, hi, master, reps = 1.0, 20.0, 4711, 40
     kw = dict(arrival_rate=lam, n_requests=n, batch_size=B, n_servers=S, flush_partial=flush,
-              bins=bb.BinRule(k=k), service=bb.ServiceSpec("uniform", lo, hi))
+              bins=bb.BinRule(k=k), service=bb.ServiceSpec("uniform", lo, hi), max_batch_wait=W)
     if pe > 0:
         kw["error"] = bb.ErrorSpec("symmetric", pe)
     t = bb.RunTemplate(**kw)
@@ -117,8 +125,9 @@ def test_replication_quantiles_bit_exact(case):
         a, s, u = replica_streams(master, r, n, lam, lo, hi, pe > 0 and k > 1)
         cfg = dict(arrival_rate=lam, n_requests=n, batch_size=B, n_servers=S,
                    flush_partial=flush, edges=edges, lo=lo, hi=hi, service="arrays",
-                   error="symmetric" if pe > 0 else "perfect", p_error=pe)
+                   error="symmetric" if pe > 0 else "perfect", p_error=pe, max_batch_wait=W)
         m, _ = O.run(O.oracle(), cfg, inputs=dict(arrivals=a, services=s, u_err=u), detail=False)
+        assert got[0, r] == pytest.approx(m["throughput"], rel=1e-12), (r, got[:, r], m)
         assert got[2, r] == m["latency_p50"], (r, got[2, r], m["latency_p50"])
         assert got[3, r] == m["latency_p99"], (r, got[3, r], m["latency_p99"])
         # the other metrics: same completions, reassociated sums
