@@ -306,6 +306,7 @@ struct SimSpec {  // a validated, materialised SimConfig
   double lo, hi, rate, lin_a, lin_b, mu, sigma;
   std::vector<double> table;
   int rng;
+  double mbw = 0.0;  // max_batch_wait (0: none)
   uint64_t k() const { return edges.size() - 1; }
   bool error_draws() const {
     return (err_kind == BB_ERR_SYMMETRIC && k() > 1 && p != 0) || err_kind == BB_ERR_CONFUSION;
@@ -360,6 +361,7 @@ SimSpec make_spec(const bb_sim_config* c, bool single = true) {
   if (!(c->arrival_rate > 0)) raise(BB_EINVAL, "sim config: arrival rate must be positive (or overload)");
   if (c->has_max_batch_wait && !(c->max_batch_wait > 0))
     raise(BB_EINVAL, "sim config: max_batch_wait must be positive");
+  s.mbw = c->has_max_batch_wait ? c->max_batch_wait : 0.0;
   const uint64_t k = c->n_edges - 1;
   s.err_kind = c->error_kind;
   s.p = c->p_error;
@@ -400,7 +402,6 @@ SimSpec make_spec(const bb_sim_config* c, bool single = true) {
   if (!single) return s;
   // the GPU envelope (SURVEY §8f lists these as the next rows)
   if (c->n_servers >= (1ull << 32)) raise(BB_EUNSUPPORTED, "n_servers must be < 2^32");
-  if (c->has_max_batch_wait) raise(BB_EUNSUPPORTED, "max_batch_wait is not implemented on the GPU path yet");
   if (k > BB_TRACE_MAX_BINS) raise(BB_EUNSUPPORTED, "more than 32 bins is not supported for single runs");
   if (c->n_requests >= (1ull << 32) - 1) raise(BB_EUNSUPPORTED, "n_requests must be < 2^32");
   return s;
@@ -606,6 +607,7 @@ void run_pipeline(const SimSpec& c, const double* a_dev, const double* s_dev, co
   A.s = s_dev;
   A.u_err = u_dev;
   A.pred = pred_dev;
+  A.max_batch_wait = c.mbw;
   if (A.err_kind && !u_dev) raise(BB_EINVAL, "trace arrays: the error model needs u_err (or pred_bin)");
   DetailDev D;
   const uint64_t cap = n;
@@ -877,8 +879,6 @@ void build_sweep(std::vector<bb_run_template> tpl, Sweep& W, cudaStream_t st, bo
   for (auto& t : W.tpl) {
     W.spec.push_back(materialize(t, 0));
     const SimSpec& s = W.spec.back();
-    if (t.has_max_batch_wait && !generated)
-      raise(BB_EUNSUPPORTED, "max_batch_wait with reference streams is not implemented on the GPU path yet");
     if (t.has_max_batch_wait && !(t.max_batch_wait > 0))
       raise(BB_EINVAL, "sim config: max_batch_wait must be positive");  // simulator.hpp:160-161
     if (!generated) continue;

@@ -17,6 +17,9 @@
 // (fp64); per-request scratch pb8 (u8) + rank (u32); per-batch SoA records.
 #include <algorithm>
 #include <cstdio>
+
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 #include <cstring>
 #include <vector>
 
@@ -1463,6 +1466,192 @@ __global__ void __launch_bounds__(1024) sel_refine_kernel(SelState* S,
   }
 }
 
+// -------------------------------------------------------- max_batch_wait
+// Timers (simulator.hpp:200-201,223-235) with strictly increasing arrivals:
+// a bin's batch starting at its front f closes at the B-th member's arrival
+// if that comes no later than a_f + W (an arrival at exactly the due time is
+// processed first: rank 1 < 2), otherwise at a_f + W with the members that
+// arrived by then; the bin is then empty, so the next batch starts at the
+// next arrival.  The segmentation depends only on the bin's own arrivals.
+// The last open batch of a bin forms at its due time, or -- with flush, if
+// the due time is after the last arrival -- at the last arrival (on_drain).
+// Dispatch order = formation order; at equal times the reference's event
+// sequence puts the timer (armed earlier) before a formation scheduled by an
+// arrival, and both before the drains, which run in bin order.
+enum : uint32_t { TM_TIMER = 0, TM_FULL = 1, TM_DRAIN = 2 };
+
+__global__ void tie_kernel(const double* __restrict__ a, uint32_t n, uint32_t* flag) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x + 1;
+  if (i < n && a[i] == a[i - 1]) *flag = 1;
+}
+
+// list[binoff[b] + rank[i]] = i: every bin's requests in arrival order
+__global__ void bin_list_kernel(const uint8_t* __restrict__ pb8, const uint32_t* __restrict__ rank,
+                                const uint32_t* __restrict__ binoff, uint32_t n, uint32_t* list) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) list[binoff[pb8[i] - 1] + rank[i]] = i;
+}
+
+// One warp per bin walks its list in 32-request chunks; records are written
+// bin-major (slot binoff[b] + j for the bin's j-th batch), and segj maps each
+// list position to j.
+struct TmArgs {
+  const double* a;
+  const double* s;
+  const uint32_t* list;
+  const uint32_t* binoff;
+  const uint32_t* bincnt;
+  uint32_t B;
+  double W, a_last;
+  int32_t flush;
+  double* recF;      // formation time
+  double* recS;      // service = max member service
+  uint32_t* recP;    // first list position (bin-relative)
+  uint32_t* recN;    // members
+  uint8_t* recB;     // bin (0-based)
+  unsigned long long* key1;  // formation time bits (~0: unused slot)
+  uint32_t* key2;            // event class << 8 | bin
+  uint32_t* segj;    // per list position
+  uint32_t* nrec;    // per bin
+};
+
+__global__ void __launch_bounds__(32) tm_segment_kernel(TmArgs T) {
+  const uint32_t b = blockIdx.x, lane = threadIdx.x;
+  const uint32_t off = T.binoff[b], cnt = T.bincnt[b];
+  uint32_t nseg = 0, f = 0;
+  bool open = false;
+  double due = 0.0, smax = 0.0;
+  auto emit = [&](double formed, uint32_t cls, uint32_t size) {
+    if (lane == 0) {
+      const uint32_t q = off + nseg;
+      T.recF[q] = formed;
+      T.recS[q] = smax;
+      T.recP[q] = f;
+      T.recN[q] = size;
+      T.recB[q] = (uint8_t)b;
+      T.key1[q] = (unsigned long long)__double_as_longlong(formed);
+      T.key2[q] = (cls << 8) | b;
+    }
+    ++nseg;
+    open = false;
+  };
+  for (uint32_t base = 0; base < cnt; base += 32) {
+    const uint32_t p = base + lane;
+    const bool valid = p < cnt;
+    const uint32_t idx = valid ? T.list[off + p] : 0;
+    const double av = valid ? T.a[idx] : CUDART_INF;
+    const double sv = valid ? T.s[idx] : 0.0;
+    const uint32_t cend = min(base + 32, cnt);
+    uint32_t q = base;  // next position to place (warp-uniform)
+    while (q < cend) {
+      if (!open) {
+        f = q;
+        due = __dadd_rn(__shfl_sync(0xffffffffu, av, q - base), T.W);  // armed at the front's arrival
+        smax = 0.0;
+        open = true;
+      }
+      const uint32_t over = __ballot_sync(0xffffffffu, valid && p >= q && av > due);
+      uint32_t lim = min(cend, f + T.B);
+      if (over) lim = min(lim, base + (uint32_t)(__ffs(over) - 1));
+      // members [q, lim): segment id and the running service max
+      double m = (p >= q && p < lim) ? sv : 0.0;
+      if (p >= q && p < lim) T.segj[off + p] = nseg;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+      smax = fmax(smax, m);
+      q = lim;
+      if (q == f + T.B) {  // the B-th member arrived first: formation at its arrival
+        emit(__shfl_sync(0xffffffffu, av, q - 1 - base), TM_FULL, T.B);
+      } else if (over && q < cend) {  // the timer fired first
+        emit(due, TM_TIMER, q - f);
+      }
+    }
+  }
+  if (open) {  // the bin's last batch: its timer, or the drain at the last arrival
+    if (T.flush && due > T.a_last) emit(T.a_last, TM_DRAIN, cnt - f);
+    else emit(due, TM_TIMER, cnt - f);
+  }
+  if (lane == 0) T.nrec[b] = nseg;
+  for (uint32_t j = nseg + lane; j < cnt; j += 32) T.key1[off + j] = ~0ull;  // unused slots sort last
+}
+
+__global__ void tm_gather_keys(const unsigned long long* __restrict__ src, const uint32_t* __restrict__ idx,
+                               uint32_t m, unsigned long long* dst) {
+  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < m) dst[j] = src[idx[j]];
+}
+
+// dispatch-ordered records: (R, S, bin, size), map[record] = position
+__global__ void tm_gather_kernel(const uint32_t* __restrict__ order, const uint8_t* __restrict__ recB,
+                                 const double* __restrict__ recF, const double* __restrict__ recS,
+                                 const uint32_t* __restrict__ recN, uint32_t nb, double* dR, double* dS,
+                                 uint8_t* dBin, uint32_t* dSize, uint32_t* map) {
+  const uint32_t d = blockIdx.x * blockDim.x + threadIdx.x;
+  if (d >= nb) return;
+  const uint32_t q = order[d];
+  dR[d] = recF[q];
+  dS[d] = recS[q];
+  if (dBin) dBin[d] = (uint8_t)(recB[q] + 1);
+  dSize[d] = recN[q];
+  map[q] = d;
+}
+
+// per request: completion, batch, members, latency key (as request_kernel)
+__global__ void __launch_bounds__(256) tm_request_kernel(
+    const double* __restrict__ a, const uint8_t* __restrict__ pb8, const uint32_t* __restrict__ rank,
+    const uint32_t* __restrict__ binoff, const uint32_t* __restrict__ segj,
+    const uint32_t* __restrict__ recP, const uint32_t* __restrict__ map,
+    const double* __restrict__ finish, const uint32_t* __restrict__ dfirst, uint32_t n,
+    unsigned long long* key_out, double* lat_part, unsigned long long* kminmax, double* completion,
+    uint32_t* batch, uint32_t* members) {
+  __shared__ double s_sum[8];
+  __shared__ unsigned long long s_min[8], s_max[8];
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double lat = 0.0;
+  unsigned long long kmin = KEY_UNSERVED, kmax = 0;
+  if (i < n) {
+    const uint32_t off = binoff[pb8[i] - 1], r = rank[i];
+    const uint32_t q = off + segj[off + r];
+    const uint32_t d = map[q];
+    const double comp = finish[d];
+    lat = __dsub_rn(comp, a[i]);  // simulator.hpp:294
+    const unsigned long long key = (unsigned long long)__double_as_longlong(lat);
+    kmin = kmax = key;
+    if (members) members[dfirst[d] + (r - recP[q])] = i;
+    key_out[i] = key;
+    if (completion) completion[i] = comp;
+    if (batch) batch[i] = d;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    lat += __shfl_xor_sync(0xffffffffu, lat, o);
+    const unsigned long long x = __shfl_xor_sync(0xffffffffu, kmin, o);
+    const unsigned long long y = __shfl_xor_sync(0xffffffffu, kmax, o);
+    kmin = x < kmin ? x : kmin;
+    kmax = y > kmax ? y : kmax;
+  }
+  if (lane == 0) {
+    s_sum[w] = lat;
+    s_min[w] = kmin;
+    s_max[w] = kmax;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double sm = 0.0;
+    for (int q = 0; q < 8; ++q) {
+      sm += s_sum[q];
+      kmin = s_min[q] < kmin ? s_min[q] : kmin;
+      kmax = s_max[q] > kmax ? s_max[q] : kmax;
+    }
+    lat_part[blockIdx.x] = sm;
+    if (kmin != KEY_UNSERVED) {
+      atomicMin(&kminmax[0], kmin);
+      atomicMax(&kminmax[1], kmax);
+    }
+  }
+}
+
 // ------------------------------------------------------------------ host
 #define BB_CK(x)                                                                        \
   do {                                                                                  \
@@ -1575,6 +1764,9 @@ void trace_run(const TraceArgs& A, TraceResult* R, cudaStream_t s) {
   double *dR = nullptr, *dS = nullptr, *start = nullptr, *finish = nullptr;
   uint32_t *map = nullptr, *order = nullptr, *dfirst = nullptr, *dsize = nullptr;
   uint8_t *dbin = nullptr, *split = nullptr;
+  bool tm = false;  // max_batch_wait timer path
+  unsigned long long nc_run = 0;
+  uint32_t *tm_list = nullptr, *tm_off = nullptr, *tm_segj = nullptr, *tm_recP = nullptr;
   BB_CK(cudaEventCreate(&ev0));
   BB_CK(cudaEventCreate(&ev1));
   BB_CK(cudaEventCreate(&ev2));
@@ -1659,36 +1851,162 @@ void trace_run(const TraceArgs& A, TraceResult* R, cudaStream_t s) {
     goto cleanup;
   }
   R->path = (int32_t)info.path;
+  // max_batch_wait: overload with flush drains every bin at t = 0, so the
+  // timers go stale and the plain pipeline applies; otherwise the timer path
+  tm = A.max_batch_wait > 0 && !(info.path == 1 && A.flush);
+  if (tm) {
+    uint32_t* tflag;
+    uint32_t htie = 0;
+    BB_CK(pool.alloc((void**)&tflag, 4));
+    BB_CK(cudaMemsetAsync(tflag, 0, 4, s));
+    if (n > 1) tie_kernel<<<grid_for(n - 1, 256), 256, 0, s>>>(A.a, n, tflag);
+    note_launch();
+    BB_CK(cudaGetLastError());
+    BB_CK(cudaMemcpyAsync(&htie, tflag, 4, cudaMemcpyDeviceToHost, s));
+    BB_CK(cudaStreamSynchronize(s));
+    if (htie) {
+      R->status = BB_EUNSUPPORTED;
+      snprintf(R->message, sizeof R->message,
+               "max_batch_wait with equal arrival times is not supported yet");
+      goto cleanup;
+    }
+  }
   {
-    const uint32_t nb = info.nb;
+    uint32_t nb = info.nb;
+    if (tm) {  // ---- timer path: per-bin segmentation, sort by formation
+      std::vector<uint32_t> hoff(k), hcnt(k), hn(k);
+      uint32_t acc = 0;
+      for (uint32_t b = 0; b < k; ++b) {
+        hcnt[b] = info.F[b] * B + info.rem[b];
+        hoff[b] = acc;
+        acc += hcnt[b];
+      }
+      uint32_t *d_off, *d_cnt, *list, *segj, *nrec, *recP, *recN, *key2, *key2b, *val, *valb;
+      uint8_t* recB;
+      unsigned long long *key1, *key1b;
+      double *recF, *recS, a_last = 0;
+      BB_CK(pool.alloc((void**)&d_off, (size_t)k * 4));
+      BB_CK(pool.alloc((void**)&d_cnt, (size_t)k * 4));
+      BB_CK(pool.alloc((void**)&nrec, (size_t)k * 4));
+      BB_CK(pool.alloc((void**)&list, (size_t)n * 4));
+      BB_CK(pool.alloc((void**)&segj, (size_t)n * 4));
+      BB_CK(pool.alloc((void**)&recP, (size_t)n * 4));
+      BB_CK(pool.alloc((void**)&recN, (size_t)n * 4));
+      BB_CK(pool.alloc((void**)&recB, (size_t)n));
+      BB_CK(pool.alloc((void**)&recF, (size_t)n * 8));
+      BB_CK(pool.alloc((void**)&recS, (size_t)n * 8));
+      BB_CK(pool.alloc((void**)&key1, (size_t)n * 8));
+      BB_CK(pool.alloc((void**)&key1b, (size_t)n * 8));
+      BB_CK(pool.alloc((void**)&key2, (size_t)n * 4));
+      BB_CK(pool.alloc((void**)&key2b, (size_t)n * 4));
+      BB_CK(pool.alloc((void**)&val, (size_t)n * 4));
+      BB_CK(pool.alloc((void**)&valb, (size_t)n * 4));
+      BB_CK(cudaMemcpyAsync(d_off, hoff.data(), (size_t)k * 4, cudaMemcpyHostToDevice, s));
+      BB_CK(cudaMemcpyAsync(d_cnt, hcnt.data(), (size_t)k * 4, cudaMemcpyHostToDevice, s));
+      BB_CK(cudaMemcpyAsync(&a_last, A.a + n - 1, 8, cudaMemcpyDeviceToHost, s));
+      BB_CK(cudaStreamSynchronize(s));
+      bin_list_kernel<<<grid_for(n, 256), 256, 0, s>>>(ws.pb8, ws.rank, d_off, n, list);
+      note_launch();
+      BB_CK(cudaGetLastError());
+      {
+        TmArgs T{A.a, A.s, list, d_off, d_cnt, B, A.max_batch_wait, a_last, A.flush,
+                 recF, recS, recP, recN, recB, key1, key2, segj, nrec};
+        tm_segment_kernel<<<k, 32, 0, s>>>(T);
+        note_launch();
+        BB_CK(cudaGetLastError());
+      }
+      BB_CK(cudaMemcpyAsync(hn.data(), nrec, (size_t)k * 4, cudaMemcpyDeviceToHost, s));
+      BB_CK(cudaStreamSynchronize(s));
+      nb = 0;
+      for (uint32_t b = 0; b < k; ++b) {
+        nb += hn[b];
+        R->per_bin[b] = hn[b];
+      }
+      // dispatch order: stable radix sorts, event class | bin first, then time
+      {
+        std::vector<uint32_t> iota(n);
+        for (uint32_t i = 0; i < n; ++i) iota[i] = i;
+        BB_CK(cudaMemcpyAsync(val, iota.data(), (size_t)n * 4, cudaMemcpyHostToDevice, s));
+        cub::DoubleBuffer<uint32_t> k2(key2, key2b), v2(val, valb);
+        size_t tb1 = 0, tb2 = 0;
+        void* tmp = nullptr;
+        BB_CK(cub::DeviceRadixSort::SortPairs(nullptr, tb1, k2, v2, (int)n, 0, 16, s));
+        cub::DoubleBuffer<unsigned long long> k1(key1, key1b);
+        BB_CK(cub::DeviceRadixSort::SortPairs(nullptr, tb2, k1, v2, (int)n, 0, 64, s));
+        BB_CK(pool.alloc(&tmp, std::max(tb1, tb2)));
+        // the time keys must follow the first sort's permutation: sort
+        // (class|bin, (time, index)) then (time, index) -- gather time by index
+        BB_CK(cub::DeviceRadixSort::SortPairs(tmp, tb1, k2, v2, (int)n, 0, 16, s));
+        note_launch();
+        uint32_t* perm = v2.Current();
+        // key1 in the class|bin order
+        unsigned long long* k1p = k1.Alternate();
+        tm_gather_keys<<<grid_for(n, 256), 256, 0, s>>>(key1, perm, n, k1p);
+        note_launch();
+        BB_CK(cudaGetLastError());
+        k1.selector ^= 1;
+        BB_CK(cub::DeviceRadixSort::SortPairs(tmp, tb2, k1, v2, (int)n, 0, 64, s));
+        note_launch();
+        order = v2.Current();
+      }
+      BB_CK(pool.alloc((void**)&map, (size_t)n * 4 + 4));
+      BB_CK(pool.alloc((void**)&dfirst, (size_t)nb * 4 + 4));
+      BB_CK(pool.alloc((void**)&dR, (size_t)nb * 8 + 8));
+      BB_CK(pool.alloc((void**)&dS, (size_t)nb * 8 + 8));
+      BB_CK(pool.alloc((void**)&dsize, (size_t)nb * 4 + 4));
+      BB_CK(pool.alloc((void**)&split, nb + 1));
+      if (nb) tm_gather_kernel<<<grid_for(nb, 256), 256, 0, s>>>(order, recB, recF, recS, recN, nb, dR, dS,
+                                                                 A.bat_bin, dsize, map);
+      note_launch();
+      BB_CK(cudaGetLastError());
+      if (A.bat_size && nb)
+        BB_CK(cudaMemcpyAsync(A.bat_size, dsize, (size_t)nb * 4, cudaMemcpyDeviceToDevice, s));
+      {
+        size_t tb = 0;
+        void* tmp = nullptr;
+        BB_CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, dsize, dfirst, (int)nb, s));
+        BB_CK(pool.alloc(&tmp, tb));
+        if (nb) BB_CK(cub::DeviceScan::ExclusiveSum(tmp, tb, dsize, dfirst, (int)nb, s));
+        note_launch();
+      }
+      tm_list = list;
+      tm_off = d_off;
+      tm_segj = segj;
+      tm_recP = recP;
+      nc_run = n;  // every request completes: drained, or formed by its timer
+    } else {
+      BB_CK(pool.alloc((void**)&map, (size_t)nb * 4 + 4));
+      BB_CK(pool.alloc((void**)&order, (size_t)nb * 4 + 4));
+      BB_CK(pool.alloc((void**)&dfirst, (size_t)nb * 4 + 4));
+      BB_CK(pool.alloc((void**)&dR, (size_t)nb * 8 + 8));
+      BB_CK(pool.alloc((void**)&dS, (size_t)nb * 8 + 8));
+      BB_CK(pool.alloc((void**)&split, nb + 1));
+      for (uint32_t b = 0; b < k; ++b) R->per_bin[b] = info.nbat[b];
+      nc_run = info.nc;
+    }
     R->n_batches = nb;
-    R->n_completed = info.nc;
-    for (uint32_t b = 0; b < k; ++b) R->per_bin[b] = info.nbat[b];
+    R->n_completed = nc_run;
     // nb == 0 (nothing served, finish() :283) still runs the request pass so
     // every request reports kNoBatch / NaN completion
-    BB_CK(pool.alloc((void**)&map, (size_t)nb * 4 + 4));
-    BB_CK(pool.alloc((void**)&order, (size_t)nb * 4 + 4));
-    BB_CK(pool.alloc((void**)&dfirst, (size_t)nb * 4 + 4));
-    BB_CK(pool.alloc((void**)&dR, (size_t)nb * 8 + 8));
-    BB_CK(pool.alloc((void**)&dS, (size_t)nb * 8 + 8));
-    BB_CK(pool.alloc((void**)&split, nb + 1));
     start = A.bat_start;
     finish = A.bat_finish;
     if (!start) BB_CK(pool.alloc((void**)&start, (size_t)nb * 8 + 8));
     if (!finish) BB_CK(pool.alloc((void**)&finish, (size_t)nb * 8 + 8));
-    if (info.path == 1 && info.nclose) {
+    if (!tm && info.path == 1 && info.nclose) {
       ovl_first_kernel<<<grid_for(info.nclose, 256), 256, 0, s>>>(ws, info.nclose);
       note_launch();
       BB_CK(cudaGetLastError());
     }
-    if (nb) order_kernel<<<grid_for(nb, 256), 256, 0, s>>>(ws, map, order, dfirst, k, B, A.flush,
-                                                   (int32_t)info.path);
-    note_launch();
-    BB_CK(cudaGetLastError());
-    if (nb) gather_kernel<<<grid_for(nb, 256), 256, 0, s>>>(ws, order, (int32_t)info.path, B, dR, dS,
-                                                    A.bat_bin, A.bat_size);
-    note_launch();
-    BB_CK(cudaGetLastError());
+    if (!tm) {
+      if (nb) order_kernel<<<grid_for(nb, 256), 256, 0, s>>>(ws, map, order, dfirst, k, B, A.flush,
+                                                     (int32_t)info.path);
+      note_launch();
+      BB_CK(cudaGetLastError());
+      if (nb) gather_kernel<<<grid_for(nb, 256), 256, 0, s>>>(ws, order, (int32_t)info.path, B, dR, dS,
+                                                      A.bat_bin, A.bat_size);
+      note_launch();
+      BB_CK(cudaGetLastError());
+    }
     double *busy_sum, *last_dev;
     BB_CK(pool.alloc((void**)&busy_sum, 8));
     BB_CK(pool.alloc((void**)&last_dev, 8));
@@ -1796,7 +2114,12 @@ void trace_run(const TraceArgs& A, TraceResult* R, cudaStream_t s) {
       Q.completion = A.req_completion;
       Q.batch = A.req_batch;
       Q.members = A.members;
-      request_kernel<<<qb, 256, 0, s>>>(Q);
+      if (tm)
+        tm_request_kernel<<<qb, 256, 0, s>>>(A.a, ws.pb8, ws.rank, tm_off, tm_segj, tm_recP, map, finish,
+                                             dfirst, n, keys, lat_part, kminmax, A.req_completion,
+                                             A.req_batch, A.members);
+      else
+        request_kernel<<<qb, 256, 0, s>>>(Q);
       note_launch();
       BB_CK(cudaGetLastError());
       sum_kernel<<<1, 256, 0, s>>>(lat_part, qb, lat_sum);
@@ -1817,7 +2140,7 @@ void trace_run(const TraceArgs& A, TraceResult* R, cudaStream_t s) {
     BB_CK(cudaMemcpyAsync(&lsum, lat_sum, 8, cudaMemcpyDeviceToHost, s));
     BB_CK(cudaMemcpyAsync(mm, kminmax, 16, cudaMemcpyDeviceToHost, s));
     BB_CK(cudaStreamSynchronize(s));
-    const unsigned long long nc = info.nc;
+    const unsigned long long nc = nc_run;
     if (nc > 0) {  // finish(), simulator.hpp:283-301
       R->makespan = last - a0;
       R->throughput = (double)nc / R->makespan;

@@ -17,6 +17,7 @@ struct TraceArgs {
   const double* s;           // services
   const double* u_err;       // nullable
   const uint8_t* pred;       // nullable, overrides the error model
+  double max_batch_wait;     // > 0: timers (simulator.hpp:200-201,223-235); 0: none
   // detail outputs (device, nullable)
   uint8_t* req_true_bin;
   uint8_t* req_pred_bin;   // copy of the partition's predicted bins

@@ -118,8 +118,9 @@ def test_replay_trace_validation():
 
 
 def test_outside_gpu_envelope_is_reported():
+    # single runs support up to 32 bins (host-side check, before any device work)
     with pytest.raises(NotImplementedError):
-        bb.run_simulation(cfg(max_batch_wait=1.5))
+        bb.run_simulation(cfg(bins=bb.uniform_boundaries(33, 1.0, 20.0)))
 
 
 @pytest.mark.skipif(os.environ.get("CUDA_VISIBLE_DEVICES", None) is None and False, reason="")

@@ -33,6 +33,16 @@ CASES = [
          servers=7),
     dict(arrival_rate=math.inf, n_requests=6400, batch_size=8, k=3, seed=80, flush=False,
          servers=3000),  # heap beyond shared memory
+    # max_batch_wait (simulator.hpp:200-201,223-235): test_simulator.cpp:244-263 shape ...
+    dict(arrival_rate=2.0, n_requests=400, batch_size=10, k=4, seed=70, servers=8, mbw=1.5),
+    # ... and larger: timers and full batches mixed, flush / no flush, errors, 3 servers
+    dict(arrival_rate=1.2, n_requests=60000, batch_size=16, k=8, seed=5, mbw=9.0,
+         error=("symmetric", 0.1)),
+    dict(arrival_rate=0.7, n_requests=30001, batch_size=32, k=4, seed=6, mbw=4.0, flush=False),
+    dict(arrival_rate=2.5, n_requests=20000, batch_size=8, k=3, seed=7, mbw=0.75, servers=3),
+    dict(arrival_rate=0.2, n_requests=5000, batch_size=4, k=1, seed=8, mbw=30.0),
+    dict(arrival_rate=math.inf, n_requests=12807, batch_size=128, k=5, seed=81, flush=True,
+         mbw=2.0),  # overload + flush: every bin drains at t = 0, the timers go stale
 ]
 
 
@@ -49,10 +59,11 @@ def configs(c):
                         batch_size=c["batch_size"], bins=bb.BinConfig(edges), error_model=em,
                         service=bb.Uniform(1.0, 20.0), seed=c["seed"],
                         flush_partial=c.get("flush", True), rng="reference",
-                        n_servers=c.get("servers", 1))
+                        n_servers=c.get("servers", 1), max_batch_wait=c.get("mbw"))
     ref = dict(arrival_rate=c["arrival_rate"], n_requests=c["n_requests"],
                batch_size=c["batch_size"], edges=edges, lo=1.0, hi=20.0, seed=c["seed"],
-               flush_partial=c.get("flush", True), n_servers=c.get("servers", 1), **od)
+               flush_partial=c.get("flush", True), n_servers=c.get("servers", 1),
+               max_batch_wait=c.get("mbw"), **od)
     return ours, ref
 
 
@@ -71,6 +82,13 @@ def test_run_simulation_detailed_matches_reference_binary(i):
     assert same_bits(b["start_time"], dr["bat_start"])
     assert same_bits(b["formed_time"], dr["bat_formed"])
     assert same_bits(b["members"], dr["members"])
+    assert same_bits(b["size"], dr["bat_size"]) and same_bits(b["bin"], dr["bat_bin"])
+    served = dr["req_batch"] != np.uint64(2**64 - 1)  # kNoBatch (simulator.hpp:35)
+    assert np.array_equal(np.asarray(r["batch"])[served].astype(np.uint64), dr["req_batch"][served])
+    if c_mbw := CASES[i].get("mbw"):  # the reference's own timer test (test_simulator.cpp:257-262)
+        assert res.metrics.n_completed == ours.n_requests
+        formed = np.asarray(b["formed_time"])[np.asarray(r["batch"], dtype=np.int64)]
+        assert np.all(formed - np.asarray(r["arrival"]) <= c_mbw + 1e-9)
     m = res.metrics
     n = ours.n_requests
     for key in ("makespan", "throughput", "latency_p50", "latency_p99"):
@@ -165,3 +183,30 @@ def test_acceptance_criterion10_curve_exact():
                              replications=10, seed=1001, rng="reference")
     got = [f"{p.throughput_mean:.4g}" for p in bb.run_experiment(spec)]
     assert got == ["0.6538", "0.807", "1.009", "1.338", "1.751", "2.355"]
+
+
+def test_run_point_reference_streams_with_timers_bit_exact():
+    # run_point (experiment.hpp:254-307) with max_batch_wait over the
+    # reference's own streams: per-replication metrics equal the binary's
+    t = bb.RunTemplate(arrival_rate=1.5, n_requests=4000, batch_size=16, n_servers=2,
+                       max_batch_wait=3.0, bins=bb.BinRule(k=4),
+                       service=bb.ServiceSpec("uniform", 1.0, 20.0))
+    p = bb.run_point(t, 99, 6, rng="reference")
+    thr, p99 = [], []
+    for r in range(6):
+        mr, _ = O.run(O.reference(), dict(arrival_rate=1.5, n_requests=4000, batch_size=16,
+                                          n_servers=2, max_batch_wait=3.0,
+                                          edges=bb.uniform_boundaries(4, 1.0, 20.0).edges,
+                                          lo=1.0, hi=20.0, seed=bb.replication_seed(99, r)),
+                      detail=False)
+        thr.append(mr["throughput"])
+        p99.append(mr["latency_p99"])
+    mean = 0.0
+    for x in thr:
+        mean += x
+    mean /= 6
+    assert same_bits(p.throughput_mean, mean)
+    m99 = 0.0
+    for x in p99:
+        m99 += x
+    assert same_bits(p.latency_p99, m99 / 6)
