@@ -73,6 +73,8 @@ struct Info {
   unsigned long long dreq[BB_TRACE_MAX_BINS];  // overload+flush: requests before bin b's drain
   uint32_t pfirst[BB_TRACE_MAX_BINS];     // fast path: members offset of bin b's partial
   uint32_t cfirst[BB_TRACE_MAX_BINS];     // overload: closing index of batch (b,0)
+  uint32_t tpos[BB_TRACE_MAX_BINS];       // overload + timers: timer batch position after the closings
+  uint32_t treq[BB_TRACE_MAX_BINS];       //   ... and requests in timer batches before it
 };
 
 struct WS {
@@ -436,16 +438,19 @@ __global__ void __launch_bounds__(TB) partition_kernel(PartArgs P) {
 
 // Drain partials, batch counts, dispatch-order bases (one warp).
 __global__ void finalize_kernel(WS ws, const double* a, uint32_t n, uint32_t k, uint32_t B,
-                                int32_t flush) {
+                                int32_t flush, double mbw) {
   const uint32_t lane = threadIdx.x;
   Info* I = ws.info;
   const uint32_t fl = *ws.flags;
+  // overload without flush but with max_batch_wait: the partial batches form
+  // when their timers fire at W (simulator.hpp:223-235)
+  const bool tmo = !(fl & FL_NOT_ALL_EQUAL) && !(fl & FL_NONMONO) && !flush && mbw > 0;
   uint32_t F = 0, rem = 0, part = 0;
   if (lane < k) {
     const uint32_t cnt = (uint32_t)ws.fin_cnt[lane];
     F = cnt / B;
     rem = cnt - F * B;
-    part = flush && rem > 0;
+    part = (flush || tmo) && rem > 0;
   }
   auto scan = [&](uint32_t v) {
     uint32_t x = v;
@@ -481,14 +486,14 @@ __global__ void finalize_kernel(WS ws, const double* a, uint32_t n, uint32_t k, 
     I->cfirst[lane] = 0xFFFFFFFFu;
     if (part) {  // on_drain partial: formed at the last arrival (simulator.hpp:203-205,220)
       const uint32_t q = nclose + (ip - part);
-      ws.recR[q] = a[n - 1];
+      ws.recR[q] = tmo ? mbw : a[n - 1];  // (or by its timer at W)
       ws.recS[q] = __longlong_as_double((long long)ws.fin_open[lane]);
       ws.recBin[q] = (uint8_t)(lane + 1);
       ws.recJ[q] = F;
       ws.recC[q] = 0xFFFFFFFFu;
     }
   }
-  unsigned long long ncl = lane < k ? (unsigned long long)F * B + (flush ? rem : 0) : 0;
+  unsigned long long ncl = lane < k ? (unsigned long long)F * B + ((flush || tmo) ? rem : 0) : 0;
   for (int o = 16; o; o >>= 1) ncl += __shfl_xor_sync(0xffffffffu, ncl, o);
   if (lane == 0) {
     I->nclose = nclose;
@@ -501,6 +506,13 @@ __global__ void finalize_kernel(WS ws, const double* a, uint32_t n, uint32_t k, 
   }
 }
 
+// overload + timers: every bin's first arrival (rank 0 in its bin)
+__global__ void first_arrival_kernel(const uint8_t* __restrict__ pb8, const uint32_t* __restrict__ rank,
+                                     uint32_t n, uint32_t* first) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n && rank[i] == 0 && pb8[i]) first[pb8[i] - 1] = i;
+}
+
 // Overload: closing index of each bin's first batch (round-0 order key).
 __global__ void ovl_first_kernel(WS ws, uint32_t nclose) {
   const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
@@ -511,7 +523,7 @@ __global__ void ovl_first_kernel(WS ws, uint32_t nclose) {
 // path 0: closing order, partials after (App. A.2 strictly increasing arrivals)
 // path 1: one tie group (overload): rounds in first-closing order, drains.
 __global__ void order_kernel(WS ws, uint32_t* map, uint32_t* order, uint32_t* dfirst,
-                             uint32_t k, uint32_t B, int32_t flush, int32_t path) {
+                             uint32_t k, uint32_t B, int32_t flush, int32_t path, int32_t tmo) {
   const Info* I = ws.info;
   const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= I->nb) return;
@@ -524,7 +536,10 @@ __global__ void order_kernel(WS ws, uint32_t* map, uint32_t* order, uint32_t* df
     before = partial ? I->pfirst[b] : (unsigned long long)q * B;
   } else {
     const uint32_t Fb = I->F[b];
-    if (partial) {
+    if (partial && tmo) {  // timer batches at W, after every t = 0 formation
+      pos = I->nclose + I->tpos[b];
+      before = (unsigned long long)B * I->nclose + I->treq[b];
+    } else if (partial) {
       pos = I->Z + I->dbase[b] + (Fb ? Fb - 1 : 0);
       before = I->dreq[b] + (unsigned long long)B * (Fb ? Fb - 1 : 0);
     } else if (flush && j >= 1) {
@@ -1764,7 +1779,8 @@ void trace_run(const TraceArgs& A, TraceResult* R, cudaStream_t s) {
   double *dR = nullptr, *dS = nullptr, *start = nullptr, *finish = nullptr;
   uint32_t *map = nullptr, *order = nullptr, *dfirst = nullptr, *dsize = nullptr;
   uint8_t *dbin = nullptr, *split = nullptr;
-  bool tm = false;  // max_batch_wait timer path
+  bool tm = false;   // max_batch_wait timer path
+  bool tmo = false;  // overload without flush, with timers: partials at W
   unsigned long long nc_run = 0;
   uint32_t *tm_list = nullptr, *tm_off = nullptr, *tm_segj = nullptr, *tm_recP = nullptr;
   BB_CK(cudaEventCreate(&ev0));
@@ -1818,7 +1834,7 @@ void trace_run(const TraceArgs& A, TraceResult* R, cudaStream_t s) {
   }
   BB_CK(cudaEventRecord(ev1, s));
   if (A.req_pred_bin) BB_CK(cudaMemcpyAsync(A.req_pred_bin, ws.pb8, n, cudaMemcpyDeviceToDevice, s));
-  finalize_kernel<<<1, 32, 0, s>>>(ws, A.a, n, k, B, A.flush);
+  finalize_kernel<<<1, 32, 0, s>>>(ws, A.a, n, k, B, A.flush, A.max_batch_wait);
   note_launch();
   BB_CK(cudaGetLastError());
   BB_CK(cudaMemcpyAsync(&info, ws.info, sizeof(Info), cudaMemcpyDeviceToHost, s));
@@ -1853,7 +1869,49 @@ void trace_run(const TraceArgs& A, TraceResult* R, cudaStream_t s) {
   R->path = (int32_t)info.path;
   // max_batch_wait: overload with flush drains every bin at t = 0, so the
   // timers go stale and the plain pipeline applies; otherwise the timer path
-  tm = A.max_batch_wait > 0 && !(info.path == 1 && A.flush);
+  tm = A.max_batch_wait > 0 && info.path != 1;
+  tmo = A.max_batch_wait > 0 && info.path == 1 && !A.flush;
+  if (tmo) {
+    // fire order at W: timers armed at the bins' first arrivals (bins that
+    // never filled a batch), then those re-armed by each bin's last
+    // round-robin formation (its position among the t = 0 batches)
+    uint32_t* dfa;
+    std::vector<uint32_t> fa(k, 0);
+    BB_CK(pool.alloc((void**)&dfa, (size_t)k * 4));
+    BB_CK(cudaMemsetAsync(dfa, 0, (size_t)k * 4, s));
+    if (info.nclose) ovl_first_kernel<<<grid_for(info.nclose, 256), 256, 0, s>>>(ws, info.nclose);
+    first_arrival_kernel<<<grid_for(n, 256), 256, 0, s>>>(ws.pb8, ws.rank, n, dfa);
+    note_launch(2);
+    BB_CK(cudaGetLastError());
+    BB_CK(cudaMemcpyAsync(fa.data(), dfa, (size_t)k * 4, cudaMemcpyDeviceToHost, s));
+    BB_CK(cudaMemcpyAsync(info.cfirst, ws.info->cfirst, sizeof info.cfirst, cudaMemcpyDeviceToHost, s));
+    BB_CK(cudaStreamSynchronize(s));
+    std::vector<std::pair<unsigned long long, uint32_t>> keyb;
+    for (uint32_t b = 0; b < k; ++b) {
+      if (!info.rem[b]) continue;
+      const uint32_t Fb = info.F[b];
+      unsigned long long key = fa[b];
+      if (Fb) {  // position of batch (b, Fb-1) in the round-robin order (order_kernel, no flush)
+        const uint32_t j = Fb - 1;
+        unsigned long long p = 0;
+        for (uint32_t q = 0; q < k; ++q) {
+          p += info.F[q] < j ? info.F[q] : j;
+          p += (info.cfirst[q] < info.cfirst[b]) && (info.F[q] > j);
+        }
+        key = (unsigned long long)n + p;
+      }
+      keyb.push_back({key, b});
+    }
+    std::sort(keyb.begin(), keyb.end());
+    uint32_t req = 0;
+    for (uint32_t x = 0; x < keyb.size(); ++x) {
+      info.tpos[keyb[x].second] = x;
+      info.treq[keyb[x].second] = req;
+      req += info.rem[keyb[x].second];
+    }
+    BB_CK(cudaMemcpyAsync(ws.info->tpos, info.tpos, sizeof info.tpos, cudaMemcpyHostToDevice, s));
+    BB_CK(cudaMemcpyAsync(ws.info->treq, info.treq, sizeof info.treq, cudaMemcpyHostToDevice, s));
+  }
   if (tm) {
     uint32_t* tflag;
     uint32_t htie = 0;
@@ -1992,14 +2050,14 @@ void trace_run(const TraceArgs& A, TraceResult* R, cudaStream_t s) {
     finish = A.bat_finish;
     if (!start) BB_CK(pool.alloc((void**)&start, (size_t)nb * 8 + 8));
     if (!finish) BB_CK(pool.alloc((void**)&finish, (size_t)nb * 8 + 8));
-    if (!tm && info.path == 1 && info.nclose) {
+    if (!tm && !tmo && info.path == 1 && info.nclose) {
       ovl_first_kernel<<<grid_for(info.nclose, 256), 256, 0, s>>>(ws, info.nclose);
       note_launch();
       BB_CK(cudaGetLastError());
     }
     if (!tm) {
       if (nb) order_kernel<<<grid_for(nb, 256), 256, 0, s>>>(ws, map, order, dfirst, k, B, A.flush,
-                                                     (int32_t)info.path);
+                                                     (int32_t)info.path, (int32_t)tmo);
       note_launch();
       BB_CK(cudaGetLastError());
       if (nb) gather_kernel<<<grid_for(nb, 256), 256, 0, s>>>(ws, order, (int32_t)info.path, B, dR, dS,

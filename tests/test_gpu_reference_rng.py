@@ -43,6 +43,14 @@ CASES = [
     dict(arrival_rate=0.2, n_requests=5000, batch_size=4, k=1, seed=8, mbw=30.0),
     dict(arrival_rate=math.inf, n_requests=12807, batch_size=128, k=5, seed=81, flush=True,
          mbw=2.0),  # overload + flush: every bin drains at t = 0, the timers go stale
+    # overload without flush: the partial batches form when their timers fire at W,
+    # in arming order (first arrivals, then each bin's last round-robin formation)
+    dict(arrival_rate=math.inf, n_requests=12807, batch_size=128, k=5, seed=82, flush=False,
+         mbw=2.0),
+    dict(arrival_rate=math.inf, n_requests=3003, batch_size=256, k=8, seed=83, flush=False,
+         mbw=1e5, error=("symmetric", 0.2)),  # bins that never fill a batch; idle until W
+    dict(arrival_rate=math.inf, n_requests=9001, batch_size=64, k=4, seed=84, flush=False,
+         mbw=3.0, servers=3),
 ]
 
 
