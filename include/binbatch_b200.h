@@ -80,7 +80,7 @@ typedef struct bb_sim_config {
   uint64_t n_servers;      /* S >= 1 (Philox generated mode: S > 1 needs a finite rate) */
   uint64_t seed;
   int32_t flush_partial;   /* default 1 */
-  int32_t has_max_batch_wait; /* GPU path: 0 */
+  int32_t has_max_batch_wait; /* timers, simulator.hpp:70 */
   double max_batch_wait;
   const double* edges;     /* k+1 strictly increasing, top may be +inf */
   uint64_t n_edges;

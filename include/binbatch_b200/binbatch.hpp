@@ -14,9 +14,10 @@
 //   * SimConfig::rng selects the random streams: Rng::reference reproduces the
 //     reference's mt19937_64 streams (bit-exact SimResult), Rng::philox (the
 //     default for sweeps) draws counter-based streams on the device
-//     (distribution-equal; generated-mode p50/p99 are not tracked).
-//   * n_servers > 1, max_batch_wait and > 32 bins (single runs) throw
-//     std::logic_error("...not implemented on the GPU path yet").
+//     (distribution-equal; every replication's p50/p99 is exact for its draws).
+//   * > 32 bins (single runs), > 64 bins (sweeps), n >= 2^32 and tie groups
+//     of equal arrivals in given trace arrays (other than the overload case)
+//     throw std::logic_error("...not supported yet").
 
 #include <algorithm>
 #include <cmath>
