@@ -166,7 +166,7 @@ __device__ __forceinline__ uint32_t fold(Rep& R, uint64_t* __restrict__ slot, do
     const double fin = dispatch<MS, !Q>(R, sv, svc_of_key_t<SVC>(svc, km >> kCntBits), B);
     if (track) *osum = 0.0;
     if (Q) {
-      q.F[id] = fin;
+      q.F[(size_t)id * kQFStride] = fin;
       const double lo = __dsub_rn(fin, R.t), hi = __dsub_rn(fin, *osum);
       if (lo < q.lm[0]) q.lm[0] = lo;    // closing member: the batch's smallest latency
       if (hi > q.lm[32]) q.lm[32] = hi;  // bounds the first member's (it arrived later)
@@ -334,10 +334,11 @@ __global__ void __launch_bounds__(kGenThreads, Q ? 2 : BB_GEN_MINB) gen_kernel(c
         if (Q) {
           q.A = L.qA + qwarp * L.q_n * 32 + lane * kQRun;
           q.Id = L.qI + qwarp * L.q_n * 32 + lane * kQRun;
-          q.F = L.qF + qslot * L.q_nf;
+          q.F = kQFStride == 1 ? L.qF + qslot * L.q_nf : L.qF + qwarp * L.q_nf * 32 + lane;
           q.lm = reinterpret_cast<double*>(s_bid + (size_t)kmax * 32) + lane;
           q.lm[0] = CUDART_INF;
           q.lm[32] = 0.0;
+
         }
         Servers srv{MS && P.n_servers ? P.n_servers : 1u, nullptr, 0};
         if (MS && srv.S > 1) {  // all servers idle at t = 0
@@ -378,7 +379,7 @@ __global__ void __launch_bounds__(kGenThreads, Q ? 2 : BB_GEN_MINB) gen_kernel(c
             st[bb * 32 + lane] = 0;
             if (track) s_osum[bb * 32 + lane] = 0.0;
             if (Q) {
-              q.F[s_bid[bb * 32 + lane]] = fin;
+              q.F[(size_t)s_bid[bb * 32 + lane] * kQFStride] = fin;
               const double lo = __dsub_rn(fin, best), hi = __dsub_rn(fin, s_osum[bb * 32 + lane]);
               if (lo < q.lm[0]) q.lm[0] = lo;
               if (hi > q.lm[32]) q.lm[32] = hi;
@@ -527,14 +528,14 @@ __global__ void __launch_bounds__(kGenThreads, Q ? 2 : BB_GEN_MINB) gen_kernel(c
             if (flush) {  // on_drain partials at the last arrival, bin order
               const double fin = dispatch<MS, !Q>(R, srv, svc_of_key_t<SVC>(svc, s0 >> kCntBits), cnt);
               if (Q) {
-                q.F[s_bid[b * 32 + lane]] = fin;
+                q.F[(size_t)s_bid[b * 32 + lane] * kQFStride] = fin;
                 const double lo = __dsub_rn(fin, R.t), hi = __dsub_rn(fin, s_osum[b * 32 + lane]);
                 if (lo < q.lm[0]) q.lm[0] = lo;
                 if (hi > q.lm[32]) q.lm[32] = hi;
               }
             } else {
               leftover += s_osum[b * 32 + lane];
-              if (Q) q.F[s_bid[b * 32 + lane]] = BB_QNAN;  // never completes
+              if (Q) q.F[(size_t)s_bid[b * 32 + lane] * kQFStride] = BB_QNAN;  // never completes
             }
           }
         }
@@ -762,15 +763,12 @@ __global__ void __launch_bounds__(kGenThreads, Q ? 2 : BB_GEN_MINB) gen_kernel(c
         double v50, v99;
         if (!OVL) {
           double* A_l = L.qA + qwarp * L.q_n * 32 + l * kQRun;
+          const uint32_t* I_l = L.qI + qwarp * L.q_n * 32 + l * kQRun;
+          const double* F_l = kQFStride == 1 ? L.qF + ls * L.q_nf : L.qF + qwarp * L.q_nf * 32 + l;
           double sum = 0.0;  // latency_mean from the latencies themselves
-#if BB_QWRITE
-          QSrcLog<true> first{A_l, L.qI + qwarp * L.q_n * 32 + l * kQRun, L.qF + ls * L.q_nf, n, lane};
-          const QSrcLat rest{A_l, n, lane};
-          q_select(first, rest, m, lmin, lmax, wreg, qregion, q_ans, lane, v50, v99, &sum);
-#else
-          const QSrcLog<false> src{A_l, L.qI + qwarp * L.q_n * 32 + l * kQRun, L.qF + ls * L.q_nf, n, lane};
-          q_select(src, src, m, lmin, lmax, wreg, qregion, q_ans, lane, v50, v99, &sum);
-#endif
+          const QSrcLog<false> src{A_l, I_l, F_l, n, lane};
+          const QFast qf{L.qK + qwarp * L.q_n * 32 + l * kQRun, A_l, I_l, F_l, n, lane};
+          q_select(src, src, m, lmin, lmax, wreg, qregion, q_ans, lane, v50, v99, &sum, &qf);
           if (lane == l) lat_out = sum / (double)m;
         } else {
           const uint32_t nb = __shfl_sync(kQFull, q_nb, l);
@@ -824,7 +822,7 @@ cudaError_t launch_gen(const GenLaunch& L, cudaStream_t s) {
   const bool blist = OVL && (MS || Q), rlog = Q && !OVL;
   const uint64_t q_n = rlog ? ((uint64_t)L.n_max + 31) & ~31ull : 0, q_nf = rlog ? L.nf_max : 0;
   const uint64_t per_thread = (blist ? (uint64_t)L.nb_max * (sizeof(double) + sizeof(uint16_t)) : 0) +
-                              (rlog ? q_n * 12 + q_nf * sizeof(double) : 0);
+                              (rlog ? q_n * 14 + q_nf * sizeof(double) : 0);
   bool held = false;
   if (per_thread) {
     // quantile mode may use most of HBM (a 10^5-request log is 0.9 MB per
@@ -835,7 +833,7 @@ cudaError_t launch_gen(const GenLaunch& L, cudaStream_t s) {
     grid = (unsigned)(grid < max_grid ? grid : max_grid);
     const uint64_t slots = (uint64_t)grid * kGenThreads;
     const uint64_t nbl = blist ? slots * L.nb_max : 0;
-    const uint64_t bytes = nbl * (sizeof(double) + sizeof(uint16_t)) + slots * (q_n * 12 + q_nf * 8) + 1024;
+    const uint64_t bytes = nbl * (sizeof(double) + sizeof(uint16_t)) + slots * (q_n * 14 + q_nf * 8) + 2048;
     unsigned char* base = nullptr;
     e = gen_scratch_acquire(bytes, s, reinterpret_cast<void**>(&base));
     if (e != cudaSuccess) return e;
@@ -852,6 +850,7 @@ cudaError_t launch_gen(const GenLaunch& L, cudaStream_t s) {
       L2.qA = reinterpret_cast<double*>(carve(slots * q_n * sizeof(double)));
       L2.qF = reinterpret_cast<double*>(carve(slots * q_nf * sizeof(double)));
       L2.qI = reinterpret_cast<uint32_t*>(carve(slots * q_n * sizeof(uint32_t)));
+      L2.qK = reinterpret_cast<uint16_t*>(carve(slots * q_n * sizeof(uint16_t)));
     }
     if (blist) L2.ovM = reinterpret_cast<uint16_t*>(carve(nbl * sizeof(uint16_t)));
     L2.q_n = q_n;

@@ -60,6 +60,7 @@ struct GenLaunch {
   uint32_t nf_max;          // most batches of any point (n/B + k + 1)
   double* qA;               // request log: arrivals (set by gen_run; layout in bb_quantile.cuh)
   uint32_t* qI;             //   batch ids
+  uint16_t* qK;             //   level-0 histogram bucket per request (selection scratch)
   double* qF;               //   completion per batch id [slot][q_nf]
   uint64_t q_n, q_nf;
 };

@@ -74,6 +74,12 @@ constexpr int kQChunk = BB_QCHUNK;  // request-log sources: runs per pipelined s
 #define BB_QRUN 32
 #endif
 constexpr uint32_t kQRun = BB_QRUN;
+// completions by batch id: a row per lane (stride 1) or the warp's 32 rows
+// interleaved (stride 32: lanes closing batches together store nearby)
+#ifndef BB_QFSTRIDE
+#define BB_QFSTRIDE 1
+#endif
+constexpr uint32_t kQFStride = BB_QFSTRIDE;
 __host__ __device__ __forceinline__ size_t qlog_index(uint32_t i) {
   return (size_t)(i / kQRun) * (32 * kQRun) + (i % kQRun);
 }
@@ -113,13 +119,13 @@ struct QSrcLog {
       }
       if (t0 + kQChunk < nt) load(t0 + kQChunk);
 #pragma unroll
-      for (int u = 0; u < kQChunk; ++u) fin[u] = id[u] != 0xFFFFFFFFu ? F[id[u]] : BB_QNAN;
+      for (int u = 0; u < kQChunk; ++u) fin[u] = id[u] != 0xFFFFFFFFu ? F[(size_t)id[u] * kQFStride] : BB_QNAN;
 #pragma unroll
       for (int u = 0; u < kQChunk; ++u) {
         const double x = __dsub_rn(fin[u], a[u]);
         const uint32_t t = t0 + u;
         if (WRITE && t < nt) A[qlog_index(t * 32 + lane)] = x;  // later passes read QSrcLat
-        f(x, isnan(x) ? 0u : 1u);
+        f(x, isnan(x) ? 0u : 1u, t * 32 + lane);
       }
     }
   }
@@ -148,7 +154,7 @@ struct QSrcLat {
       for (int u = 0; u < kQChunk; ++u) x[u] = nx[u];
       if (t0 + kQChunk < nt) load(t0 + kQChunk);
 #pragma unroll
-      for (int u = 0; u < kQChunk; ++u) f(x[u], isnan(x[u]) ? 0u : 1u);
+      for (int u = 0; u < kQChunk; ++u) f(x[u], isnan(x[u]) ? 0u : 1u, (t0 + u) * 32 + lane);
     }
   }
 };
@@ -172,8 +178,59 @@ struct QSrcBatches {
         w[u] = i < nb ? M[(size_t)i * stride] : 0u;
       }
 #pragma unroll
-      for (int u = 0; u < kQGroup; ++u) f(x[u], w[u]);
+      for (int u = 0; u < kQGroup; ++u) f(x[u], w[u], (t0 + u) * 32 + lane);
     }
+  }
+};
+
+// Fast collection for the request log: the first pass leaves every request's
+// level-0 histogram bucket (u16, 0xFFFF: not completed) in the log layout, so
+// the collect pass scans 2 B per request -- eight requests per lane and load
+// -- and keeps only the indices of requests in the wanted buckets; their
+// latencies are then gathered with independent loads.
+struct QFast {
+  uint16_t* Bk;         // the replication's buckets (+ qlog_index(i))
+  const double* A;      // its arrivals
+  const uint32_t* Id;   // its batch ids
+  const double* F;      // its completions by batch id
+  uint32_t n, lane;
+
+  // indices of the requests whose bucket is one of want[0..3] (0xFFFFFFFF:
+  // unused) into slots[] as raw 64-bit words; returns how many
+  __device__ uint32_t collect(const uint32_t want[4], unsigned long long* slots) const {
+    static_assert(kQRun % 8 == 0, "eight buckets per lane load");
+    constexpr int G = 4;  // loads in flight per lane
+    const uint32_t ng = (n + 7) / 8;  // groups of 8 requests
+    uint32_t nc = 0;
+    for (uint32_t g0 = 0; g0 < ng; g0 += 32 * G) {
+      uint4 v[G];
+#pragma unroll
+      for (int u = 0; u < G; ++u) {
+        const uint32_t g = g0 + u * 32 + lane;
+        v[u] = g < ng ? *reinterpret_cast<const uint4*>(Bk + qlog_index(g * 8))
+                      : make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+      }
+#pragma unroll
+      for (int u = 0; u < G; ++u) {
+        const uint32_t w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+        for (int h = 0; h < 8; ++h) {
+          const uint32_t bk = (w[h >> 1] >> (16 * (h & 1))) & 0xFFFFu;
+          const bool hit = (bk == want[0] || bk == want[1] || bk == want[2] || bk == want[3]) &&
+                           (g0 + u * 32 + lane) * 8 + h < n;  // (padding is never written)
+          const uint32_t hm = __ballot_sync(kQFull, hit);
+          if (hit)
+            slots[nc + __popc(hm & ((1u << lane) - 1u))] =
+                (unsigned long long)((g0 + u * 32 + lane) * 8 + h);
+          nc += __popc(hm);
+        }
+      }
+    }
+    return nc;
+  }
+  __device__ double latency(uint32_t i) const {
+    const size_t o = qlog_index(i);
+    return __dsub_rn(F[(size_t)Id[o] * kQFStride], A[o]);
   }
 };
 
@@ -185,7 +242,7 @@ struct QSrcBatches {
 template <class Src1, class Src>
 __device__ void q_select(Src1& first, const Src& src, uint64_t m, double lmin, double lmax, unsigned char* region,
                          uint32_t region_bytes, double* ans, uint32_t lane, double& p50,
-                         double& p99, double* wsum) {
+                         double& p99, double* wsum, const QFast* qf = nullptr) {
   uint32_t* hist = reinterpret_cast<uint32_t*>(region);
   const uint32_t cap = ((region_bytes - 1024u) / 10u) & ~7u;  // + a 256-bucket histogram
   double* cx = reinterpret_cast<double*>(region);
@@ -201,6 +258,7 @@ __device__ void q_select(Src1& first, const Src& src, uint64_t m, double lmin, d
   double val[4];
   bool done[4];
   const uint64_t kbase = qkey(lmin), kspan = qkey(lmax) - kbase;
+  uint32_t fast_nc = 0;
   uint32_t sh0 = 0;
   while (sh0 < 63 && (kspan >> sh0) >= kQBuckets) ++sh0;
 #pragma unroll
@@ -221,14 +279,18 @@ __device__ void q_select(Src1& first, const Src& src, uint64_t m, double lmin, d
     for (uint32_t j = lane; j < kQBuckets; j += 32) hist[j] = 0;
     __syncwarp();
     const uint64_t gw = qwidth(gsh);
+    const bool keep = qf && gsh >= 64;  // level 0: remember every request's bucket
     double acc = 0.0;
-    source.for_each([&](double x, uint32_t w) {
+    source.for_each([&](double x, uint32_t w, uint32_t i) {
       if (sum && w) acc += x * (double)w;
       const uint64_t d = qkey(x) - glo;
+      uint32_t b16 = 0xFFFFu;
       if (w && d < gw) {
         const uint64_t bk = d >> s2;
-        atomicAdd(&hist[bk < kQBuckets ? bk : kQBuckets - 1], w);
+        b16 = (uint32_t)(bk < kQBuckets ? bk : kQBuckets - 1);
+        atomicAdd(&hist[b16], w);
       }
+      if (keep && i < qf->n) qf->Bk[qlog_index(i)] = (uint16_t)b16;
     });
     if (sum) {
 #pragma unroll
@@ -275,7 +337,39 @@ __device__ void q_select(Src1& first, const Src& src, uint64_t m, double lmin, d
   };
 
   refine(first, kbase, 64, wsum != nullptr);
-  for (int iter = 0; iter < 64; ++iter) {
+  // fast path: the level-0 buckets of the wanted ranks hold few enough values
+  bool fast = false;
+  if (qf) {
+    uint64_t total = 0;
+    uint32_t want[4] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu};
+    bool ok = true;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      ok &= sh[t] == sh0 && sh0 > 0;
+      bool dup = false;
+#pragma unroll
+      for (int u = 0; u < t; ++u) dup |= klo[u] == klo[t];
+      if (!dup) {
+        total += cnt[t];
+        want[t] = (uint32_t)((klo[t] - kbase) >> sh0);
+      }
+    }
+    if (ok && total <= cap) {
+      fast = true;
+      __syncwarp();  // the histogram is done with; the region holds candidates
+      unsigned long long* slots = reinterpret_cast<unsigned long long*>(cx);
+      const uint32_t ncol = qf->collect(want, slots);
+      __syncwarp();
+      for (uint32_t c = lane; c < ncol; c += 32) {
+        const double x = qf->latency((uint32_t)slots[c]);
+        cx[c] = x;
+        cw[c] = 1;
+      }
+      __syncwarp();
+      fast_nc = ncol;
+    }
+  }
+  for (int iter = 0; !fast && iter < 64; ++iter) {
     // a range of one bit pattern holds equal values: resolved without a pass
     uint64_t total = 0;
     int big = -1;
@@ -310,14 +404,14 @@ __device__ void q_select(Src1& first, const Src& src, uint64_t m, double lmin, d
   for (int t = 0; t < 4; ++t) open |= !done[t];
   if (open) {
     // collect the candidates of every open range
-    uint32_t nc = 0;
+    uint32_t nc = fast ? fast_nc : 0;
     uint64_t wlo[4], ww[4];  // open ranges (width 0: closed)
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
       wlo[t] = klo[t];
       ww[t] = done[t] ? 0ull : qwidth(sh[t]);
     }
-    src.for_each([&](double x, uint32_t w) {
+    if (!fast) src.for_each([&](double x, uint32_t w, uint32_t) {
       const uint64_t key = qkey(x);
       bool hit = false;
 #pragma unroll
