@@ -294,10 +294,26 @@ int main() {
     CHECK(approx(result.metrics.makespan, 2.0, 1e-12));
     CHECK(approx(result.metrics.throughput, 64.0 / 2.0, 1e-12));
   }
-  {  // max_batch_wait: not yet on the GPU path -- reported, not faked
-    SimConfig cfg = overload_uniform(400, 10, 4, 70);
+  {  // a batch-wait cap bounds in-bin waiting (test_simulator.cpp:244-263)
+    SimConfig cfg;
+    cfg.arrival_rate = 2.0;
+    cfg.n_requests = 400;
+    cfg.batch_size = 10;
+    cfg.bins = uniform_boundaries(4, 1.0, 20.0);
+    cfg.service = make_uniform(1.0, 20.0);
+    cfg.n_servers = 8;
+    cfg.seed = 70;
     cfg.max_batch_wait = 1.5;
-    CHECK_THROWS(run_simulation(cfg), std::logic_error);
+    const SimResult result = run_simulation_detailed(cfg);
+    CHECK(result.metrics.n_completed == 400);
+    bool any_undersized = false, waits_ok = true;
+    for (const BatchRecord& b : result.batches) {
+      any_undersized = any_undersized || b.members.size() < 10;
+      for (const std::size_t id : b.members)
+        waits_ok &= b.formed_time - result.requests[id].arrival_time <= 1.5 + 1e-9;
+    }
+    CHECK(any_undersized);
+    CHECK(waits_ok);
   }
   {  // acceptance criteria 1, 2, 7: capacity protocol (B=128, U[1,20], overload, 10 seeds)
     ExperimentSpec spec;
