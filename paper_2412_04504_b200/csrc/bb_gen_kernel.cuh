@@ -408,6 +408,7 @@ __global__ void __launch_bounds__(kGenThreads, Q ? 2 : BB_GEN_MINB) gen_kernel(c
             err_pair(u, e[u], e[u + 1]);
           }
         }
+        uint4 idh = make_uint4(0u, 0u, 0u, 0u);  // quantile mode: ids held for the next store
         // the bucket lookup is warp-uniform: one copy of the loop per path
         auto main_loop = [&](auto bk) {
           constexpr bool BK = decltype(bk)::value;
@@ -474,9 +475,15 @@ __global__ void __launch_bounds__(kGenThreads, Q ? 2 : BB_GEN_MINB) gen_kernel(c
 #pragma unroll
               for (int u = 0; u < U; u += 2)
                 *reinterpret_cast<double2*>(q.A + o + u) = make_double2(at[u], at[u + 1]);
-#pragma unroll
-              for (int u = 0; u < U; u += 4)
-                *reinterpret_cast<uint4*>(q.Id + o + u) = make_uint4(qid[u], qid[u + 1], qid[u + 2], qid[u + 3]);
+              // ids: a lane's eight consecutive ids are one 32 B sector; store
+              // them together (half-sector stores cost several times more)
+              static_assert(U == 4, "ids are held for one iteration");
+              if ((i & 4u) == 0) {
+                idh = make_uint4(qid[0], qid[1], qid[2], qid[3]);
+              } else {
+                *reinterpret_cast<uint4*>(q.Id + o - 4) = idh;
+                *reinterpret_cast<uint4*>(q.Id + o) = make_uint4(qid[0], qid[1], qid[2], qid[3]);
+              }
             }
             if (PIPE) {
 #pragma unroll
@@ -489,6 +496,7 @@ __global__ void __launch_bounds__(kGenThreads, Q ? 2 : BB_GEN_MINB) gen_kernel(c
         };
         if (bkt_ok) main_loop(std::true_type{});
         else main_loop(std::false_type{});
+        if (Q && (i & 4u)) *reinterpret_cast<uint4*>(q.Id + qlog_index(i - 4)) = idh;
         // tail: fewer than U requests left, one at a time
         for (; !failed && i < n; ++i) {
           const Draw d0 = draw<SVC>(cyc_rank, nt, i, c2, c3, cyc);
