@@ -513,6 +513,13 @@ def trace_measure(bb, torch, dev, stream, n=10_000_000):
     # partition kernel algorithmic bytes: read a,s (16) + pred (1); write pb (1) + rank (4)
     # + closing records (8+8+1+4+4 per batch = 25/B)
     part_bytes = n * (16 + 1 + 1 + 4) + (n / 16) * 25
+    traffic = None  # DRAM bytes of one partition launch, from one `ncu --set full` capture
+    prof = os.path.join(ROOT, "profiles", "r01_trace_c2_ncu.json")
+    if os.path.exists(prof):
+        caps = json.load(open(prof))
+        for c in (caps if isinstance(caps, list) else [caps]):
+            if "partition_kernel" in c.get("kernel", "") and c.get("dram_bytes_per_request"):
+                traffic = c["dram_bytes_per_request"] * n
     return {"workload": "C2: 10^7-request trace from the reference generator, k=8, B=16, "
                         "lambda=0.95 cap, Symmetric(0.1) predictions as input",
             "value": n / (t / 1e3), "unit": "requests/s", "ms_per_run": t,
@@ -521,7 +528,7 @@ def trace_measure(bb, torch, dev, stream, n=10_000_000):
                          "achieved": part_bytes / (tp / 1e3) / 1e9,
                          "peak": measured_peaks()["hbm_gbs"], "unit": "GB/s",
                          "frac": part_bytes / (tp / 1e3) / 1e9 / measured_peaks()["hbm_gbs"],
-                         "traffic": None,
+                         "traffic": traffic,
                          "algorithmic": "22 B/request + 25 B/batch (reads a,s,pred; writes bin, rank, records)"}}
 
 
