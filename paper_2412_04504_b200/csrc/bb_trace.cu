@@ -28,7 +28,10 @@
 namespace bb {
 namespace {
 
-constexpr int TB = 256, IPT = 8, TILE = TB * IPT, NW = TB / 32;
+#ifndef BB_PART_IPT
+#define BB_PART_IPT 8
+#endif
+constexpr int TB = 256, IPT = BB_PART_IPT, TILE = TB * IPT, NW = TB / 32;
 constexpr unsigned long long FLAG_A = 1ull << 62, FLAG_P = 2ull << 62, VAL_MASK = (1ull << 62) - 1;
 constexpr unsigned long long KEY_UNSERVED = ~0ull;
 constexpr uint32_t FL_NONMONO = 1, FL_TIE_GT_B = 2, FL_NOT_ALL_EQUAL = 4;
