@@ -169,3 +169,42 @@ def test_quantiles_off_leaves_nan_and_same_throughput():
     # latency_mean: the sum of the latencies themselves vs sum(completions) - sum(arrivals)
     np.testing.assert_allclose(on[1], off[1], rtol=1e-9)
     assert np.isfinite(on[2]).all() and (on[3] >= on[2]).all()
+
+
+def test_randomized_configs_bit_exact():
+    """Random shapes (B = 1 included, timers, servers, overload, errors, no
+    flush): every sampled replication's p50/p99 equals the oracle's."""
+    rng = np.random.default_rng(20241205)
+    for trial in range(40):
+        k = int(rng.integers(1, 9))
+        B = int(rng.choice([1, 2, 3, 8, 16, 40]))
+        S = int(rng.choice([1, 1, 2, 5]))
+        n = int(rng.integers(max(B, 200), 6000))
+        over = rng.random() < 0.25
+        cap = bb.throughput(B, k, 1.0, 20.0) * S
+        lam = math.inf if over else float(cap * rng.uniform(0.3, 1.3))
+        flush = bool(rng.random() < 0.6)
+        W = float(rng.uniform(0.5, 40.0)) if rng.random() < 0.5 else None
+        pe = float(rng.choice([0.0, 0.0, 0.2])) if k > 1 else 0.0
+        kw = dict(arrival_rate=lam, n_requests=n, batch_size=B, n_servers=S, flush_partial=flush,
+                  bins=bb.BinRule(k=k), service=bb.ServiceSpec("uniform", 1.0, 20.0),
+                  max_batch_wait=W)
+        if pe > 0:
+            kw["error"] = bb.ErrorSpec("symmetric", pe)
+        reps, master = 8, 1000 + trial
+        got = kernel_rep_metrics(bb.RunTemplate(**kw), reps, master)
+        edges = bb.uniform_boundaries(k, 1.0, 20.0).edges
+        for r in (0, reps - 1):
+            a, s, u = replica_streams(master, r, n, lam, 1.0, 20.0, pe > 0)
+            cfg = dict(arrival_rate=lam, n_requests=n, batch_size=B, n_servers=S,
+                       flush_partial=flush, edges=edges, lo=1.0, hi=20.0, service="arrays",
+                       error="symmetric" if pe > 0 else "perfect", p_error=pe, max_batch_wait=W)
+            m, _ = O.run(O.oracle(), cfg, inputs=dict(arrivals=a, services=s, u_err=u),
+                         detail=False)
+            ctx = (trial, r, kw)
+            if m["n_completed"] == 0:
+                assert got[2, r] == 0.0 and got[3, r] == 0.0, ctx
+                continue
+            assert got[0, r] == pytest.approx(m["throughput"], rel=1e-12), ctx
+            assert got[2, r] == m["latency_p50"], ctx
+            assert got[3, r] == m["latency_p99"], ctx
