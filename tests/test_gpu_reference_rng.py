@@ -218,3 +218,33 @@ def test_run_point_reference_streams_with_timers_bit_exact():
     for x in p99:
         m99 += x
     assert same_bits(p.latency_p99, m99 / 6)
+
+
+def test_randomized_timer_runs_match_reference_binary():
+    """Random max_batch_wait shapes through run_simulation_detailed with the
+    reference's streams: batches, completions and p50/p99 bit-identical."""
+    rng = np.random.default_rng(7)
+    for trial in range(24):
+        k = int(rng.integers(1, 9))
+        B = int(rng.choice([1, 2, 5, 16, 33]))
+        S = int(rng.choice([1, 1, 2, 4]))
+        n = int(rng.integers(max(B, 100), 5000))
+        over = rng.random() < 0.2
+        lam = math.inf if over else float(bb.throughput(B, k, 1.0, 20.0) * S * rng.uniform(0.3, 1.4))
+        flush = bool(rng.random() < 0.6)
+        W = float(rng.uniform(0.2, 30.0))
+        c = dict(arrival_rate=lam, n_requests=n, batch_size=B, k=k, seed=500 + trial,
+                 servers=S, flush=flush, mbw=W)
+        if k > 1 and rng.random() < 0.4:
+            c["error"] = ("symmetric", float(rng.uniform(0.0, 0.4)))
+        ours, ref = configs(c)
+        mr, dr = O.run(O.reference(), ref)
+        res = bb.run_simulation_detailed(ours)
+        r, b = res.requests, res.batches
+        ctx = (trial, c)
+        assert same_bits(r["completion"], dr["req_completion"]), ctx
+        assert same_bits(b["finish_time"], dr["bat_finish"]), ctx
+        assert same_bits(b["formed_time"], dr["bat_formed"]), ctx
+        assert same_bits(b["members"], dr["members"]), ctx
+        for key in ("makespan", "throughput", "latency_p50", "latency_p99"):
+            assert same_bits(getattr(res.metrics, key), mr[key]), (key, ctx)
