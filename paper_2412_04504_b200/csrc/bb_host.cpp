@@ -1020,7 +1020,17 @@ void launch_sweep(const SweepParams* E, Sweep& W, uint64_t rep_begin, uint64_t r
       }
       CK(cudaEventRecord(g_ev[0], st));
     }
-    CK(bb::gen_run(L, st));
+    const cudaError_t ge = bb::gen_run(L, st);
+    if (ge == cudaErrorMemoryAllocation && L.quant) {
+      cudaGetLastError();
+      char buf[256];
+      snprintf(buf, sizeof buf,
+               "generated-mode quantiles keep a %u-request log per replication in flight "
+               "(about 14 B per request): not even one block fits in free HBM; "
+               "bb_set_generated_quantiles(0) runs without p50/p99", nmax);
+      raise(BB_EUNSUPPORTED, buf);
+    }
+    CK(ge);
     if (time_it && first) {
       CK(cudaEventRecord(g_ev[1], st));
       g_ev_name = "gen_kernel";
