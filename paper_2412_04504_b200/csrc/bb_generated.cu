@@ -149,8 +149,8 @@ uint64_t gen_scratch_budget() {
   size_t free_b = 0, total_b = 0;
   if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) return 0;
   const uint64_t have = free_b + g_scratch[cur_dev()].bytes;
-  const uint64_t reserve = (uint64_t)8 << 30;  // leave room for the caller's own tensors
-  return have > reserve ? (uint64_t)((have - reserve) * 0.85) : 0;
+  const uint64_t reserve = (uint64_t)6 << 30;  // leave room for the caller's own tensors
+  return have > reserve ? (uint64_t)((have - reserve) * 0.92) : 0;
 }
 
 cudaError_t gen_setup_thresholds(GenPoint* pts_dev, uint32_t n_points, cudaStream_t s) {
