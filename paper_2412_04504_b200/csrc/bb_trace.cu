@@ -28,6 +28,9 @@
 namespace bb {
 namespace {
 
+#ifndef BB_PART_MATCH
+#define BB_PART_MATCH 1  // stable in-warp ranks by match_any (0: one ballot per bin)
+#endif
 #ifndef BB_PART_IPT
 #define BB_PART_IPT 8
 #endif
@@ -213,6 +216,24 @@ __global__ void __launch_bounds__(TB) partition_kernel(PartArgs P) {
 
   // stable rank within the warp's 256 consecutive requests: one ballot per bin
   uint32_t wc = 0;  // lane b: running count of bin b+1 in this warp
+#if BB_PART_MATCH
+  // peers by __match_any_sync; each bin's lowest lane publishes the bin's count
+  const uint32_t lt = lanemask_lt();
+#pragma unroll
+  for (int j = 0; j < IPT; ++j) {
+    const uint32_t peers = __match_any_sync(0xffffffffu, pb[j]);
+    const uint32_t mine = pb[j] ? peers : 0u;
+    if (lane < k) s_wcnt[w][lane] = 0;
+    __syncwarp();
+    if (pb[j] && !(mine & lt)) s_wcnt[w][pb[j] - 1] = __popc(mine);
+    __syncwarp();
+    const uint32_t own = lane < k ? s_wcnt[w][lane] : 0u;
+    __syncwarp();
+    const uint32_t basec = __shfl_sync(0xffffffffu, wc, pb[j] ? pb[j] - 1 : 0);
+    rl[j] = basec + __popc(mine & lt);
+    wc += own;
+  }
+#else
 #pragma unroll
   for (int j = 0; j < IPT; ++j) {
     uint32_t mine = 0, own = 0;
@@ -225,6 +246,7 @@ __global__ void __launch_bounds__(TB) partition_kernel(PartArgs P) {
     rl[j] = basec + __popc(mine & lanemask_lt());
     wc += __popc(own);
   }
+#endif
   if (lane < k) s_wcnt[w][lane] = wc;
   __syncthreads();
   if (tid == 0 && s_flags) atomicOr(P.ws.flags, s_flags);
