@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define BB_ABI_VERSION 1
+#define BB_ABI_VERSION 2
 #define BB_MAX_BINS 64        /* generated mode (fused kernel) */
 #define BB_TRACE_MAX_BINS 32  /* trace mode (one warp lane per bin) */
 #define BB_NO_BATCH 0xFFFFFFFFu
@@ -87,7 +87,7 @@ typedef struct bb_sim_config {
   int32_t error_kind;      /* bb_error_kind */
   int32_t service_kind;    /* bb_service_kind */
   double p_error;          /* Symmetric */
-  const double* confusion; /* Confusion: k*k row-major rows[true-1][pred-1] */
+  const double* confusion; /* Confusion: row-major rows[true-1][pred-1], confusion_k^2 */
   double lo, hi;           /* Uniform [lo,hi]; Linear len range */
   double rate;             /* Exponential */
   double lin_a, lin_b;     /* Linear: t = lin_b*len + lin_a */
@@ -96,6 +96,9 @@ typedef struct bb_sim_config {
   uint64_t n_table;
   int32_t rng;             /* bb_rng_kind */
   int32_t device;          /* CUDA ordinal; -1 = current */
+  uint64_t confusion_k;    /* rows (== columns) of `confusion`; must equal k
+                              ("sim config: confusion matrix size does not match
+                              bin count", simulator.hpp:163-165) */
 } bb_sim_config;
 
 /* SimMetrics, simulator.hpp:76-87 */
@@ -188,7 +191,8 @@ typedef struct bb_run_template {
   uint64_t n_edges;
   int32_t error_kind;
   double p_error;
-  const double* confusion;
+  const double* confusion;    /* the resolved matrix (ResolvedWorkload::confusion), row-major */
+  uint64_t confusion_k;       /* its rows (== columns); checked against the point's k */
 } bb_run_template;
 
 /* SweepAxis / ExperimentSpec, experiment.hpp:75-87 */
@@ -207,6 +211,9 @@ typedef struct bb_experiment_spec {
   uint64_t seed;
   int32_t rng;            /* bb_rng_kind: PHILOX (fused kernel) or REFERENCE
                              (the reference's streams, bit-exact, slower) */
+  const char* name;       /* ExperimentSpec::name (NULL: "experiment"); per-point
+                             failures come back as BB_ERUNTIME "experiment '<name>':
+                             sweep point <i> failed: ..." (experiment.hpp:352-358) */
 } bb_experiment_spec;
 
 /* ---------------------------------------------------------------- errors */
@@ -285,6 +292,29 @@ bb_status bb_empirical_boundaries(uint64_t k, const double* samples, uint64_t n,
 double bb_analytic_throughput(uint64_t batch_size, uint64_t k, double lo, double hi);
 double bb_analytic_latency(uint64_t batch_size, uint64_t k, double lo, double hi, double lambda);
 
+/* analytics.hpp:55-126 with the reference's argument checks (BB_EINVAL on
+ * B == 0, k == 0, !(0 <= lo < hi), a non-positive or infinite rate, ...). */
+bb_status bb_expected_service_time(uint64_t batch_size, uint64_t bins, double min_time,
+                                   double max_time, double* out);           /* :55-62 */
+bb_status bb_throughput(uint64_t batch_size, uint64_t bins, double min_time, double max_time,
+                        double* out);                                        /* :64-69 */
+bb_status bb_max_throughput(uint64_t batch_size, double min_time, double max_time,
+                            double* out);                                    /* :71-77 */
+bb_status bb_min_bins_for_throughput(uint64_t batch_size, double min_time, double max_time,
+                                     double epsilon, uint64_t* out);         /* :79-98 */
+bb_status bb_expected_latency(uint64_t batch_size, uint64_t bins, double min_time,
+                              double max_time, double arrival_rate, double* out); /* :100-108 */
+bb_status bb_exponential_service_bound(uint64_t batch_size, uint64_t bins, double rate,
+                                       double* out);                         /* :110-126 */
+/* harmonic_number, service_dist.hpp:82-87 */
+bb_status bb_harmonic_number(uint64_t n, double* out);
+/* assign_bin, binning.hpp:133-144 (host; BB_EDOMAIN outside [e_0, e_k]) */
+bb_status bb_assign_bin(const double* edges, uint64_t n_edges, double length, uint64_t* bin);
+/* brute_force_boundaries, binning.hpp:268-351: family 0 = Uniform(p0, p1),
+ * 1 = Exponential(rate p0); out holds k+1 edges */
+bb_status bb_brute_force_boundaries(uint64_t k, int32_t family, double p0, double p1,
+                                    uint64_t batch_size, uint64_t grid_points, double* out);
+
 /* Philox4x32-10 on the host (the same function the kernels inline), for
  * known-answer tests: out[4] = philox(ctr[4], key[2]). */
 void bb_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);
@@ -292,6 +322,17 @@ void bb_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out
  * 53-bit keys, on the device: table = 1 the inter-arrival gap function,
  * 0 the service-key function (accuracy tests). */
 bb_status bb_exponential_variates(const uint64_t* keys, uint64_t n, int32_t table, double* out);
+
+/* The bin edges a run template materialises to (materialize,
+ * experiment.hpp:128-146; log-normal: exp(mu + sigma*Phi^-1(j/k)) with an open
+ * top bin).  *n_edges receives k+1; out (may be NULL) must hold that many. */
+bb_status bb_template_edges(const bb_run_template* t, double* out, uint64_t capacity,
+                            uint64_t* n_edges);
+/* The service time the generated-mode kernels assign to each 53-bit service
+ * key (key = the Philox draw; cyclic traces: the table rank), on the device
+ * -- lets a test rebuild a replication's services exactly. */
+bb_status bb_service_of_keys(const bb_run_template* t, const uint64_t* keys, uint64_t n,
+                             double* out);
 
 /* Generated mode computes every replication's exact latency p50/p99 like the
  * reference's finish() (simulator.hpp:289-301), on by default.  Turning it off

@@ -154,9 +154,10 @@ def make_cfg(d: dict):
     mbw = d.get("max_batch_wait")
     c.has_max_batch_wait = int(mbw is not None)
     c.max_batch_wait = float(mbw) if mbw is not None else 0.0
-    keep.edges = np.ascontiguousarray(d["edges"], dtype=np.float64)
-    c.edges = _ptr(keep.edges, _dp)
-    c.n_edges = len(keep.edges)
+    if d.get("edges") is not None and len(d["edges"]):
+        keep.edges = np.ascontiguousarray(d["edges"], dtype=np.float64)
+        c.edges = _ptr(keep.edges, _dp)
+        c.n_edges = len(keep.edges)
     c.error_kind = ERR[d.get("error", "perfect")]
     c.p_error = float(d.get("p_error", 0.0))
     if d.get("confusion") is not None:
@@ -253,6 +254,24 @@ def run_replicas(d: dict, master: int, rep0: int, nrep: int, threads: int):
     if st != OK:
         raise OracleError(st, lib.last().decode())
     return [a.as_dict() for a in arr], secs.value
+
+
+POINT_FIELDS = ("throughput_mean", "throughput_std", "latency_mean", "latency_std", "latency_p50",
+                "latency_p99", "makespan_mean", "busy_fraction_mean", "analytic_throughput",
+                "analytic_latency", "analytic_max_throughput")
+
+
+def run_point(d: dict, k: int, master: int, reps: int) -> dict:
+    """The reference's own run_point (experiment.hpp:254-307) on the template
+    `d` describes (edges omitted -> derived from k) -> PointResult numbers."""
+    lib = reference()
+    lib.bbref_run_point.argtypes = [C.POINTER(Cfg), C.c_uint64, C.c_uint64, C.c_uint64, _dp]
+    c, keep = make_cfg(d)
+    out = np.empty(len(POINT_FIELDS))
+    st = lib.bbref_run_point(C.byref(c), k, master, reps, out.ctypes.data_as(_dp))
+    if st != OK:
+        raise OracleError(st, lib.last().decode())
+    return dict(zip(POINT_FIELDS, out.tolist()))
 
 
 def uniform_boundaries(k, lo, hi):

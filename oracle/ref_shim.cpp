@@ -235,6 +235,72 @@ int bbref_run_replicas(const bbo_config* c, uint64_t master, uint64_t rep0, uint
   return BBO_OK;
 }
 
+// run_point (experiment.hpp:254-307) of the template the config describes:
+// service uniform / exponential / trace (table = the resolved trace times,
+// ResolvedWorkload, :95-108), bins from `edges` when given, else the rule's
+// k (derived edges, :128-146).  out[] = the PointResult numbers in
+// declaration order: throughput_mean, throughput_std, latency_mean,
+// latency_std, latency_p50, latency_p99, makespan_mean, busy_fraction_mean,
+// analytic_throughput, analytic_latency, analytic_max_throughput.
+int bbref_run_point(const bbo_config* c, uint64_t k, uint64_t master, uint64_t reps, double* out) {
+  try {
+    RunTemplate t;
+    ResolvedWorkload w;
+    t.arrival_rate = c->arrival_rate;
+    t.n_requests = c->n_requests;
+    t.batch_size = c->batch_size;
+    t.n_servers = c->n_servers;
+    t.flush_partial = c->flush_partial != 0;
+    if (c->has_max_batch_wait) t.max_batch_wait = c->max_batch_wait;
+    switch (c->service_kind) {
+      case BBO_SVC_UNIFORM:
+        t.service.kind = ServiceKind::uniform;
+        t.service.min_time = c->lo;
+        t.service.max_time = c->hi;
+        break;
+      case BBO_SVC_EXPONENTIAL:
+        t.service.kind = ServiceKind::exponential;
+        t.service.rate = c->rate;
+        break;
+      case BBO_SVC_TRACE_CYCLIC:
+      case BBO_SVC_TRACE_RESAMPLE:
+        t.service.kind = ServiceKind::trace;
+        t.service.trace_mode =
+            c->service_kind == BBO_SVC_TRACE_CYCLIC ? TraceMode::cyclic : TraceMode::resample;
+        w.trace_times.assign(c->table, c->table + c->n_table);
+        break;
+      default:
+        throw std::invalid_argument("ref shim: run_point needs a uniform, exponential or trace service");
+    }
+    if (c->edges && c->n_edges >= 2) t.bins.edges.assign(c->edges, c->edges + c->n_edges);
+    else t.bins.k = k;
+    const std::size_t kk = t.bins.edges.empty() ? k : t.bins.edges.size() - 1;
+    switch (c->error_kind) {
+      case BBO_ERR_PERFECT: t.error.kind = ErrorKind::perfect; break;
+      case BBO_ERR_SYMMETRIC:
+        t.error.kind = ErrorKind::symmetric;
+        t.error.p_error = c->p_error;
+        break;
+      case BBO_ERR_CONFUSION: {
+        t.error.kind = ErrorKind::confusion;
+        std::vector<std::vector<double>> rows(kk, std::vector<double>(kk));
+        for (std::size_t i = 0; i < kk; ++i)
+          for (std::size_t j = 0; j < kk; ++j) rows[i][j] = c->confusion[i * kk + j];
+        w.confusion = make_confusion(rows);
+        break;
+      }
+    }
+    const PointResult r = run_point(t, w, master, reps);
+    const double v[] = {r.throughput_mean, r.throughput_std, r.latency_mean, r.latency_std,
+                        r.latency_p50, r.latency_p99, r.makespan_mean, r.busy_fraction_mean,
+                        r.analytic_throughput, r.analytic_latency, r.analytic_max_throughput};
+    std::memcpy(out, v, sizeof v);
+    return BBO_OK;
+  } catch (...) {
+    return code_of(std::current_exception());
+  }
+}
+
 // Closed forms (analytics.hpp), for the generated-mode parity tests.
 double bbref_throughput(uint64_t B, uint64_t k, double lo, double hi) { return throughput(B, k, lo, hi); }
 double bbref_expected_latency(uint64_t B, uint64_t k, double lo, double hi, double lam) {

@@ -285,9 +285,8 @@ def _cfg_struct(cfg: SimConfig, table=None):
     elif isinstance(em, Confusion):
         c.error_kind = 2
         keep.conf = np.ascontiguousarray(em.rows, dtype=np.float64).ravel()
-        if len(em.rows) != len(keep.edges) - 1:
-            keep.conf = None
-        c.confusion = _dptr(keep.conf) if keep.conf is not None else None
+        c.confusion = _dptr(keep.conf)
+        c.confusion_k = len(em.rows)
     else:
         c.error_kind = 0
     sv = cfg.service
@@ -548,6 +547,7 @@ def _template_struct(t: RunTemplate, keep: _Keep) -> _capi.RunTemplateC:
     if t.error.rows is not None:
         keep.conf = np.ascontiguousarray(t.error.rows, dtype=np.float64).ravel()
         c.confusion = _dptr(keep.conf)
+        c.confusion_k = len(t.error.rows)
     return c
 
 
@@ -566,6 +566,8 @@ def _spec_struct(spec: ExperimentSpec):
     E.replications = int(spec.replications)
     E.seed = int(spec.seed) & (2**64 - 1)
     E.rng = _capi.RNG[spec.rng]
+    keep.name = str(spec.name).encode()
+    E.name = keep.name
     return E, keep
 
 
@@ -599,9 +601,8 @@ def run_experiment(spec: ExperimentSpec, jobs: int = 1) -> List[PointResult]:
 
 
 def run_point(t: RunTemplate, master_seed: int, replications: int, rng: str = "philox") -> PointResult:
-    """experiment.hpp:254-307"""
-    return run_experiment(ExperimentSpec(base=t, replications=replications, seed=master_seed,
-                                         rng=rng))[0]
+    """experiment.hpp:254-307 (errors propagate unwrapped, like the reference's run_point)"""
+    return run_points([t], replications, master_seed, rng=rng)[0]
 
 
 def sweep_shard_device(spec: ExperimentSpec, rep_begin: int, rep_end: int, rep_ptr: int,
@@ -691,6 +692,28 @@ def exponential_variates(keys, table: bool = True):
     _check(_lib.bb_exponential_variates(x.ctypes.data_as(C.POINTER(C.c_uint64)), x.shape[0],
                                         int(bool(table)),
                                         out.ctypes.data_as(C.POINTER(C.c_double))))
+    return out
+
+
+def template_edges(t: RunTemplate) -> List[float]:
+    """The edges `t` materialises to (experiment.hpp:128-146)."""
+    keep = _Keep()
+    c = _template_struct(t, keep)
+    n = C.c_uint64()
+    _check(_lib.bb_template_edges(C.byref(c), None, 0, C.byref(n)))
+    out = np.empty(n.value)
+    _check(_lib.bb_template_edges(C.byref(c), _dptr(out), n.value, C.byref(n)))
+    return out.tolist()
+
+
+def service_of_keys(t: RunTemplate, keys) -> np.ndarray:
+    """The service time the generated-mode kernels give each 53-bit key."""
+    keep = _Keep()
+    c = _template_struct(t, keep)
+    x = np.ascontiguousarray(keys, dtype=np.uint64)
+    out = np.empty(x.shape[0])
+    _check(_lib.bb_service_of_keys(C.byref(c), x.ctypes.data_as(C.POINTER(C.c_uint64)),
+                                   x.shape[0], _dptr(out)))
     return out
 
 

@@ -38,7 +38,7 @@ class SimConfigC(C.Structure):
         ("p_error", C.c_double), ("confusion", _dp), ("lo", C.c_double), ("hi", C.c_double),
         ("rate", C.c_double), ("lin_a", C.c_double), ("lin_b", C.c_double), ("mu", C.c_double),
         ("sigma", C.c_double), ("table", _dp), ("n_table", C.c_uint64), ("rng", C.c_int32),
-        ("device", C.c_int32),
+        ("device", C.c_int32), ("confusion_k", C.c_uint64),
     ]
 
 
@@ -90,7 +90,7 @@ class RunTemplateC(C.Structure):
         ("lin_a", C.c_double), ("lin_b", C.c_double), ("mu", C.c_double), ("sigma", C.c_double),
         ("trace_times", _dp), ("n_trace", C.c_uint64), ("k", C.c_uint64), ("edges", _dp),
         ("n_edges", C.c_uint64), ("error_kind", C.c_int32), ("p_error", C.c_double),
-        ("confusion", _dp),
+        ("confusion", _dp), ("confusion_k", C.c_uint64),
     ]
 
 
@@ -100,7 +100,8 @@ class SweepAxisC(C.Structure):
 
 class ExperimentSpecC(C.Structure):
     _fields_ = [("base", RunTemplateC), ("axes", SweepAxisC * 2), ("n_axes", C.c_uint64),
-                ("replications", C.c_uint64), ("seed", C.c_uint64), ("rng", C.c_int32)]
+                ("replications", C.c_uint64), ("seed", C.c_uint64), ("rng", C.c_int32),
+                ("name", C.c_char_p)]
 
 
 # every symbol include/binbatch_b200.h declares (checked by tests/test_capi_symbols.py)
@@ -112,7 +113,10 @@ EXPORTS = [
     "bb_uniform_boundaries", "bb_exponential_boundaries", "bb_empirical_boundaries",
     "bb_analytic_throughput", "bb_analytic_latency", "bb_philox4x32_10", "bb_launch_count",
     "bb_last_kernel_ms", "bb_points_shard_device", "bb_run_points", "bb_points_reduce_device", "bb_transfer_bytes",
-    "bb_exponential_variates", "bb_set_generated_quantiles",
+    "bb_exponential_variates", "bb_set_generated_quantiles", "bb_template_edges",
+    "bb_service_of_keys", "bb_expected_service_time", "bb_throughput", "bb_max_throughput",
+    "bb_min_bins_for_throughput", "bb_expected_latency", "bb_exponential_service_bound",
+    "bb_harmonic_number", "bb_assign_bin", "bb_brute_force_boundaries",
 ]
 
 
@@ -166,6 +170,20 @@ def load():
     lib.bb_launch_count.argtypes = [C.c_int]
     lib.bb_last_kernel_ms.restype = C.c_double
     lib.bb_last_kernel_ms.argtypes = [P(C.c_char_p)]
+    lib.bb_template_edges.argtypes = [P(RunTemplateC), _dp, C.c_uint64, P(C.c_uint64)]
+    lib.bb_service_of_keys.argtypes = [P(RunTemplateC), P(C.c_uint64), C.c_uint64, _dp]
+    for f in ("bb_expected_service_time", "bb_throughput"):
+        getattr(lib, f).argtypes = [C.c_uint64, C.c_uint64, C.c_double, C.c_double, _dp]
+    lib.bb_max_throughput.argtypes = [C.c_uint64, C.c_double, C.c_double, _dp]
+    lib.bb_min_bins_for_throughput.argtypes = [C.c_uint64, C.c_double, C.c_double, C.c_double,
+                                               P(C.c_uint64)]
+    lib.bb_expected_latency.argtypes = [C.c_uint64, C.c_uint64, C.c_double, C.c_double,
+                                        C.c_double, _dp]
+    lib.bb_exponential_service_bound.argtypes = [C.c_uint64, C.c_uint64, C.c_double, _dp]
+    lib.bb_harmonic_number.argtypes = [C.c_uint64, _dp]
+    lib.bb_assign_bin.argtypes = [_dp, C.c_uint64, C.c_double, P(C.c_uint64)]
+    lib.bb_brute_force_boundaries.argtypes = [C.c_uint64, C.c_int32, C.c_double, C.c_double,
+                                              C.c_uint64, C.c_uint64, _dp]
     lib.bb_set_generated_quantiles.restype = C.c_int
     lib.bb_set_generated_quantiles.argtypes = [C.c_int]
     return lib

@@ -445,7 +445,7 @@ __global__ void __launch_bounds__(kGenThreads, Q ? 2 : BB_GEN_MINB) gen_kernel(c
 #pragma unroll
               for (int u = U - 1; u >= 0; --u)
                 if (out_of_support(d[u].xs)) bad = (uint32_t)u, bx = d[u].xs;
-              raise_error(L.err, i + bad, BB_EDOMAIN, svc_of_key_t<SVC>(svc, bx), r);
+              raise_error(L.err, ((uint64_t)P.gidx << 32) | (i + bad), BB_EDOMAIN, svc_of_key_t<SVC>(svc, bx), r);
               failed = true;
               break;
             }
@@ -504,7 +504,7 @@ __global__ void __launch_bounds__(kGenThreads, Q ? 2 : BB_GEN_MINB) gen_kernel(c
           err_pair(i & ~1u, e0, e1);
           if (i & 1u) e0 = e1;
           if (out_of_support(d0.xs)) {
-            raise_error(L.err, i, BB_EDOMAIN, svc_of_key_t<SVC>(svc, d0.xs), r);
+            raise_error(L.err, ((uint64_t)P.gidx << 32) | i, BB_EDOMAIN, svc_of_key_t<SVC>(svc, d0.xs), r);
             failed = true;
           } else {
             const uint32_t p0 = bin_pred(d0.xs, e0);
@@ -572,7 +572,7 @@ __global__ void __launch_bounds__(kGenThreads, Q ? 2 : BB_GEN_MINB) gen_kernel(c
           const Draw d = draw<SVC>(cyc_rank, nt, i, c2, c3, cyc);
           if ((i & 1u) == 0) err_pair(i, e0, e1);
           if (out_of_support(d.xs)) {
-            raise_error(L.err, i, BB_EDOMAIN, svc_of_key_t<SVC>(svc, d.xs), r);
+            raise_error(L.err, ((uint64_t)P.gidx << 32) | i, BB_EDOMAIN, svc_of_key_t<SVC>(svc, d.xs), r);
             failed = true;
             break;
           }

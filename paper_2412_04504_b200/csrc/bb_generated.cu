@@ -72,7 +72,10 @@ __global__ void thresholds_kernel(GenPoint* pts, uint32_t n_points) {
 }
 
 // mean_std (experiment.hpp:188-200) in replica order, bit-for-bit the
-// reference's sequential sums.  One block per point, one thread per field.
+// reference's sequential sums: every operation is an explicitly rounded
+// intrinsic, so no FMA contraction can fuse `ss += d * d` (the reference is
+// built without -march, i.e. without contraction).  One block per
+// point, one thread per field.
 __global__ void point_reduce_kernel(const double* __restrict__ rep, uint32_t n_points,
                                     uint32_t reps, double* __restrict__ out) {
   const uint32_t p = blockIdx.x, f = threadIdx.x;
@@ -81,13 +84,16 @@ __global__ void point_reduce_kernel(const double* __restrict__ rep, uint32_t n_p
   const double* x = rep + f * stride + (uint64_t)p * reps;
   const double nn = (double)reps;
   double sum = 0;
-  for (uint32_t i = 0; i < reps; ++i) sum += x[i];
-  const double mean = sum / nn;
+  for (uint32_t i = 0; i < reps; ++i) sum = __dadd_rn(sum, x[i]);
+  const double mean = __ddiv_rn(sum, nn);
   double sd = 0;
   if (reps >= 2 && (f == BB_REP_THROUGHPUT || f == BB_REP_LATENCY)) {
     double ss = 0;
-    for (uint32_t i = 0; i < reps; ++i) ss += (x[i] - mean) * (x[i] - mean);
-    sd = sqrt(ss / (nn - 1.0));
+    for (uint32_t i = 0; i < reps; ++i) {
+      const double d = __dsub_rn(x[i], mean);
+      ss = __dadd_rn(ss, __dmul_rn(d, d));
+    }
+    sd = __dsqrt_rn(__ddiv_rn(ss, __dsub_rn(nn, 1.0)));
   }
   double* o = out + (uint64_t)p * 8;
   switch (f) {
@@ -100,7 +106,35 @@ __global__ void point_reduce_kernel(const double* __restrict__ rep, uint32_t n_p
   }
 }
 
+// The service time the fused kernel assigns to each key (svc_of_key_t, the
+// same inlined function and compilation flags as bb_gen_<family>.cu): lets a
+// test rebuild a replication's services on the host (bb_service_of_keys).
+template <int KIND>
+__global__ void svc_keys_kernel(const SvcParams p, const uint64_t* __restrict__ x, uint64_t n,
+                                double* __restrict__ out) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = svc_of_key_t<KIND>(p, x[i]);
+}
+
 }  // namespace
+
+cudaError_t service_of_keys(const SvcParams& p, const uint64_t* x, uint64_t n, double* out,
+                            cudaStream_t s) {
+  if (!n) return cudaSuccess;
+  const uint64_t b = (n + 255) / 256;
+  const unsigned grid = (unsigned)(b < 4096 ? b : 4096);
+  switch (p.kind) {
+    case kSvcUniform: svc_keys_kernel<kSvcUniform><<<grid, 256, 0, s>>>(p, x, n, out); break;
+    case kSvcLinear: svc_keys_kernel<kSvcLinear><<<grid, 256, 0, s>>>(p, x, n, out); break;
+    case kSvcExponential: svc_keys_kernel<kSvcExponential><<<grid, 256, 0, s>>>(p, x, n, out); break;
+    case kSvcLogNormal: svc_keys_kernel<kSvcLogNormal><<<grid, 256, 0, s>>>(p, x, n, out); break;
+    case kSvcTable: svc_keys_kernel<kSvcTable><<<grid, 256, 0, s>>>(p, x, n, out); break;
+    default: svc_keys_kernel<kSvcCyclic><<<grid, 256, 0, s>>>(p, x, n, out); break;
+  }
+  note_launch();
+  return cudaGetLastError();
+}
 
 namespace {
 struct Scratch {

@@ -79,6 +79,9 @@ template <int SVC>
 cudaError_t gen_run_svc(const GenLaunch& L, cudaStream_t s);
 // The fused per-replica kernel.  Returns the launch error.
 cudaError_t gen_run(const GenLaunch& L, cudaStream_t s);
+// svc_of_key_t of every key (test support: bb_service_of_keys).
+cudaError_t service_of_keys(const SvcParams& p, const uint64_t* x, uint64_t n, double* out,
+                            cudaStream_t s);
 // mean_std per point over replica order (experiment.hpp:188-200, :275-281).
 // stats_out: [n_points][8] = thr mean, thr std, lat mean, lat std, p50, p99, makespan, busy
 cudaError_t gen_point_reduce(const double* rep, uint32_t n_points, uint32_t reps,

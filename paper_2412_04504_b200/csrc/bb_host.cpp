@@ -368,17 +368,26 @@ SimSpec make_spec(const bb_sim_config* c, bool single = true) {
   if (c->error_kind == BB_ERR_SYMMETRIC) {  // make_symmetric, binning.hpp:164-168
     if (!(c->p_error >= 0) || !(c->p_error <= 0.5))
       raise(BB_EINVAL, "symmetric error model: need 0 <= p_error <= 0.5");
-  } else if (c->error_kind == BB_ERR_CONFUSION) {  // make_confusion, :170-188
-    if (!c->confusion) raise(BB_EINVAL, "sim config: confusion matrix size does not match bin count");
-    s.conf.assign(c->confusion, c->confusion + k * k);
-    for (uint64_t i = 0; i < k; ++i) {
+  } else if (c->error_kind == BB_ERR_CONFUSION) {
+    // make_confusion (binning.hpp:170-188) on the matrix as given, then
+    // validate()'s size check (simulator.hpp:163-165)
+    const uint64_t ck = c->confusion_k;
+    if (!c->confusion || ck == 0) raise(BB_EINVAL, "confusion matrix: empty");
+    s.conf.assign(c->confusion, c->confusion + ck * ck);
+    for (uint64_t i = 0; i < ck; ++i) {
       double sum = 0.0;
-      for (uint64_t j = 0; j < k; ++j) {
-        if (!(s.conf[i * k + j] >= 0)) raise(BB_EINVAL, "confusion matrix: negative entry");
-        sum += s.conf[i * k + j];
+      for (uint64_t j = 0; j < ck; ++j) {
+        if (!(s.conf[i * ck + j] >= 0)) raise(BB_EINVAL, "confusion matrix: negative entry");
+        sum += s.conf[i * ck + j];
       }
-      if (std::abs(sum - 1.0) > 1e-9) raise(BB_EINVAL, "confusion matrix: row does not sum to 1");
+      if (std::abs(sum - 1.0) > 1e-9) {
+        char buf[128];
+        snprintf(buf, sizeof buf, "confusion matrix: row %llu sums to %g, expected 1",
+                 (unsigned long long)(i + 1), sum);
+        raise(BB_EINVAL, buf);
+      }
     }
+    if (ck != k) raise(BB_EINVAL, "sim config: confusion matrix size does not match bin count");
   } else if (c->error_kind != BB_ERR_PERFECT) {
     raise(BB_EINVAL, "unknown error model");
   }
@@ -740,6 +749,7 @@ SimSpec materialize(const bb_run_template& t, uint64_t seed) {
   c.error_kind = t.error_kind;
   c.p_error = t.p_error;
   c.confusion = t.confusion;
+  c.confusion_k = t.confusion_k;
   std::vector<double> edges;
   switch (t.service) {
     case BB_KIND_UNIFORM:
@@ -856,6 +866,17 @@ std::vector<bb_run_template> expand(const bb_experiment_spec* spec) {
   return pts;
 }
 
+// run_experiment's failure wrapper (experiment.hpp:352-358): a point's error
+// comes back as runtime_error "experiment '<name>': sweep point <i> failed: <what>".
+struct PointFail {
+  const char* name = nullptr;  // null: run_point semantics (no wrapping)
+  [[noreturn]] void raise_at(size_t i, bb_status st, const std::string& what) const {
+    if (!name) raise(st, what);
+    raise(BB_ERUNTIME, std::string("experiment '") + name + "': sweep point " + std::to_string(i) +
+                           " failed: " + what);
+  }
+};
+
 // Build device GenPoints for a set of templates; group launches by template
 // instantiation (error kind, cyclic, overload).
 struct Sweep {
@@ -871,16 +892,22 @@ struct SweepParams {
 
 // `generated`: the points run in the fused Philox kernel (its envelope is
 // checked); reference-stream points run the trace pipeline per replication.
-void build_sweep(std::vector<bb_run_template> tpl, Sweep& W, cudaStream_t st, bool generated = true) {
+void build_sweep(std::vector<bb_run_template> tpl, Sweep& W, cudaStream_t st, bool generated = true,
+                 const PointFail& pf = PointFail{}) {
   if (tpl.empty()) raise(BB_EINVAL, "sweep has no points");
   W.tpl = std::move(tpl);
   const size_t P = W.tpl.size();
   W.spec.reserve(P);
-  for (auto& t : W.tpl) {
-    W.spec.push_back(materialize(t, 0));
+  for (size_t i = 0; i < P; ++i) {
+    const bb_run_template& t = W.tpl[i];
+    try {
+      W.spec.push_back(materialize(t, 0));
+    } catch (const BBError& e) {
+      pf.raise_at(i, e.st, e.msg);
+    }
     const SimSpec& s = W.spec.back();
-    if (t.has_max_batch_wait && !(t.max_batch_wait > 0))
-      raise(BB_EINVAL, "sim config: max_batch_wait must be positive");  // simulator.hpp:160-161
+    if (t.has_max_batch_wait && !(t.max_batch_wait > 0))  // simulator.hpp:160-161
+      pf.raise_at(i, BB_EINVAL, "sim config: max_batch_wait must be positive");
     if (!generated) continue;
     if (s.S > 4096) raise(BB_EUNSUPPORTED, "more than 4096 servers is not supported");
     if (s.k() > BB_MAX_BINS) raise(BB_EUNSUPPORTED, "more than 64 bins is not supported");
@@ -943,7 +970,7 @@ void build_sweep(std::vector<bb_run_template> tpl, Sweep& W, cudaStream_t st, bo
 }
 
 void launch_sweep(const SweepParams* E, Sweep& W, uint64_t rep_begin, uint64_t rep_end,
-                  double* rep_dev, cudaStream_t st, bool time_it) {
+                  double* rep_dev, cudaStream_t st, bool time_it, const PointFail& pf = PointFail{}) {
   const size_t P = W.tpl.size();
   // group points by kernel instantiation; each group's points are copied
   // (already threshold-resolved) into a contiguous device array
@@ -1041,11 +1068,16 @@ void launch_sweep(const SweepParams* E, Sweep& W, uint64_t rep_begin, uint64_t r
     bb::DevError he;
     d2h(&he, err.p, sizeof he, st);
     CK(cudaStreamSynchronize(st));
-    if (he.packed != ~0ull) {
+    if (he.packed != ~0ull) {  // packed = (point << 40 | request << 8 | code)
+      const size_t pt = (size_t)(he.packed >> 40);
+      const SimSpec& s = W.spec[pt < W.spec.size() ? pt : 0];
       char buf[256];
-      snprintf(buf, sizeof buf, "assign_bin: length %.17g outside bin support (replication %llu)",
-               he.value, (unsigned long long)he.aux);
-      raise((bb_status)(he.packed & 0xFF), buf);
+      if (he.value > 0 && std::isfinite(he.value))  // binning.hpp:135-140
+        snprintf(buf, sizeof buf, "assign_bin: length %g outside bin support [%g, %g]", he.value,
+                 s.edges.front(), s.edges.back());
+      else  // simulator.hpp:189-190
+        snprintf(buf, sizeof buf, "simulation: drew a non-positive service time");
+      pf.raise_at(pt, (bb_status)(he.packed & 0xFF), buf);
     }
   }
 }
@@ -1101,7 +1133,7 @@ void fill_points(const SweepParams* E, const Sweep& W, const std::vector<double>
 
 // Bit-exact replication loop (reference streams, trace pipeline per replica).
 void reference_point_reps(const SweepParams* E, const Sweep& W, std::vector<double>& rep,
-                          cudaStream_t st) {
+                          cudaStream_t st, const PointFail& pf = PointFail{}) {
   const size_t P = W.tpl.size();
   const uint64_t R = E->replications;
   rep.assign(BB_REP_FIELDS * P * R, 0.0);
@@ -1116,8 +1148,13 @@ void reference_point_reps(const SweepParams* E, const Sweep& W, std::vector<doub
       DBuf a = upload(H.a.data(), s.n, st), sv = upload(H.s.data(), s.n, st), u;
       if (!H.u.empty()) u = upload(H.u.data(), s.n, st);
       bb_sim_metrics m;
-      run_pipeline(s, a.as<double>(), sv.as<double>(), u.as<double>(), nullptr, &m, nullptr,
-                   false, st);
+      try {
+        run_pipeline(s, a.as<double>(), sv.as<double>(), u.as<double>(), nullptr, &m, nullptr,
+                     false, st);
+      } catch (const BBError& e) {
+        if (e.st == BB_EUNSUPPORTED) throw;
+        pf.raise_at(i, e.st, e.msg);
+      }
       const uint64_t o = i * R + r, stride = P * R;
       rep[BB_REP_THROUGHPUT * stride + o] = m.throughput;
       rep[BB_REP_LATENCY * stride + o] = m.latency_mean;
@@ -1130,20 +1167,20 @@ void reference_point_reps(const SweepParams* E, const Sweep& W, std::vector<doub
 }
 
 void run_points_host(std::vector<bb_run_template> tpl, SweepParams E, int32_t rng,
-                     bb_point_result* out) {
+                     bb_point_result* out, const PointFail& pf = PointFail{}) {
   const int dev = current_device(-1);
   std::lock_guard<std::mutex> lock(g_ctx[dev].mu);
   cudaStream_t st = ctx_stream(dev);
   Sweep W;
-  build_sweep(std::move(tpl), W, st, rng != BB_RNG_REFERENCE);
+  build_sweep(std::move(tpl), W, st, rng != BB_RNG_REFERENCE, pf);
   const uint64_t P = W.tpl.size(), R = E.replications;
   DBuf rep(BB_REP_FIELDS * P * R * 8, st), stats(P * 8 * 8, st);
   if (rng == BB_RNG_REFERENCE) {
     std::vector<double> h;
-    reference_point_reps(&E, W, h, st);
+    reference_point_reps(&E, W, h, st, pf);
     CK(cudaMemcpyAsync(rep.p, h.data(), h.size() * 8, cudaMemcpyHostToDevice, st));
   } else {
-    launch_sweep(&E, W, 0, R, rep.as<double>(), st, true);
+    launch_sweep(&E, W, 0, R, rep.as<double>(), st, true, pf);
   }
   CK(bb::gen_point_reduce(rep.as<double>(), (uint32_t)P, (uint32_t)R, stats.as<double>(), st));
   std::vector<double> hs(P * 8);
@@ -1181,6 +1218,10 @@ void points_reduce(std::vector<bb_run_template> tpl, SweepParams E, const double
 }
 
 }  // namespace
+
+namespace bb {
+void set_last_error(const std::string& msg) { g_err = msg; }
+}  // namespace bb
 
 // =================================================================== C ABI
 extern "C" {
@@ -1284,7 +1325,9 @@ bb_status bb_run_experiment(const bb_experiment_spec* spec, unsigned jobs, bb_po
     if (n_points) *n_points = P;
     if (!out) return;
     if (capacity < P) raise(BB_EINVAL, "bb_run_experiment: output capacity too small");
-    run_points_host(std::move(tpl), SweepParams{spec->seed, spec->replications}, spec->rng, out);
+    PointFail pf;
+    pf.name = spec->name ? spec->name : "experiment";
+    run_points_host(std::move(tpl), SweepParams{spec->seed, spec->replications}, spec->rng, out, pf);
   });
 }
 
@@ -1300,13 +1343,13 @@ bb_status bb_run_points(const bb_run_template* points, uint64_t n_points, uint64
 
 bb_status bb_run_point(const bb_run_template* t, uint64_t master_seed, uint64_t replications,
                        bb_point_result* out) {
-  bb_experiment_spec E{};
-  if (t) E.base = *t;
-  E.n_axes = 0;
-  E.replications = replications;
-  E.seed = master_seed;
-  uint64_t np = 0;
-  return bb_run_experiment(t ? &E : nullptr, 1, out, 1, &np);
+  // run_point (experiment.hpp:254): errors propagate unwrapped
+  return guarded([&] {
+    if (!t || !out) raise(BB_EINVAL, "bb_run_point: null template or output");
+    if (replications < 1) raise(BB_EINVAL, "experiment spec: replications must be >= 1");
+    run_points_host(std::vector<bb_run_template>(1, *t), SweepParams{master_seed, replications},
+                    BB_RNG_PHILOX, out);
+  });
 }
 
 bb_status bb_sweep_shard_device(const bb_experiment_spec* spec, uint64_t rep_begin,
@@ -1389,6 +1432,36 @@ bb_status bb_exponential_variates(const uint64_t* keys, uint64_t n, int32_t tabl
     cudaStream_t st = ctx_stream(dev);
     DBuf x = upload(keys, n, st), y(n * 8, st);
     CK(bb::exp1_variates(x.as<uint64_t>(), n, table, y.as<double>(), st));
+    d2h(out, y.p, n * 8, st);
+    CK(cudaStreamSynchronize(st));
+  });
+}
+
+bb_status bb_template_edges(const bb_run_template* t, double* out, uint64_t capacity,
+                            uint64_t* n_edges) {
+  return guarded([&] {
+    if (!t) raise(BB_EINVAL, "null run template");
+    const SimSpec s = materialize(*t, 0);
+    if (n_edges) *n_edges = s.edges.size();
+    if (!out) return;
+    if (capacity < s.edges.size()) raise(BB_EINVAL, "bb_template_edges: capacity too small");
+    std::memcpy(out, s.edges.data(), s.edges.size() * 8);
+  });
+}
+
+bb_status bb_service_of_keys(const bb_run_template* t, const uint64_t* keys, uint64_t n,
+                             double* out) {
+  return guarded([&] {
+    if (!t) raise(BB_EINVAL, "null run template");
+    if (n && (!keys || !out)) raise(BB_EINVAL, "service keys: null buffer");
+    const SimSpec c = materialize(*t, 0);
+    const int dev = current_device(-1);
+    std::lock_guard<std::mutex> lock(g_ctx[dev].mu);
+    cudaStream_t st = ctx_stream(dev);
+    SvcDev sv;
+    make_svc(c, sv, st);
+    DBuf x = upload(keys, n, st), y(n * 8, st);
+    CK(bb::service_of_keys(sv.p, x.as<uint64_t>(), n, y.as<double>(), st));
     d2h(out, y.p, n * 8, st);
     CK(cudaStreamSynchronize(st));
   });

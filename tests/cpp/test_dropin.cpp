@@ -1,9 +1,8 @@
 // The reference's simulator unit tests (proj/tests/test_simulator.cpp) and
 // acceptance criteria 1/2/7/8/10 (proj/tests/acceptance.cpp), rewritten
 // against the C++ drop-in header: the only change a reference user makes is
-// the include (binbatch_b200/binbatch.hpp) and the link line.  The
-// max_batch_wait case checks that the GPU path reports it as not yet
-// implemented (std::logic_error) instead of silently falling back.
+// the include (binbatch_b200/binbatch.hpp) and the link line.  (The
+// reference's own test programs also run unchanged: tests/cpp/Makefile.)
 #include <algorithm>
 #include <cmath>
 #include <cstdio>

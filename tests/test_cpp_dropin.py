@@ -60,3 +60,50 @@ def test_output_formats_byte_identical_to_reference(tmp_path):
     b = subprocess.run([mine_exe], capture_output=True, check=True).stdout
     assert a == b
     assert a.count(b"\n") == 6 + 1 + 3
+
+
+BIN = os.path.join(ROOT, "tests", "cpp", "_bin")
+
+
+def _suite(name):
+    exe = os.path.join(BIN, name)
+    if not os.path.exists(exe):
+        pytest.skip(f"{exe} not built (make -C tests/cpp needs /root/reference)")
+    return exe
+
+
+def test_reference_unit_suite_pins_the_catch2_shim():
+    """The shim runner on the reference's own unit tests, built against the
+    reference headers (CPU only): all 84 test cases pass."""
+    r = subprocess.run([_suite("unit_tests_ref")], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-4000:]
+    assert "All tests passed" in r.stdout and "in 84 test cases" in r.stdout
+
+
+def test_reference_unit_suite_host_cases_pass_on_cpu():
+    """Without a GPU every simulation call fails loudly (no CPU path); every
+    test case that stays on the host (edges, analytics, predict_bin, traces,
+    JSON specs) passes against the drop-in unchanged."""
+    r = subprocess.run([_suite("unit_tests_b200")], capture_output=True, text=True, timeout=600,
+                       env=dict(os.environ, CUDA_VISIBLE_DEVICES=""))
+    fails = [l for l in r.stdout.splitlines() if l.strip().startswith("FAILED")]
+    assert all("CUDA" in l or "cuda" in l for l in fails), "\n".join(fails[:20])
+
+
+@pytest.mark.gpu
+def test_reference_acceptance_suite_unchanged_on_gpu():
+    """proj/tests/acceptance.cpp, unchanged, against the drop-in: 10/10."""
+    r = subprocess.run([_suite("acceptance_b200")], capture_output=True, text=True, timeout=900)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "10/10 criteria passed" in r.stdout
+
+
+@pytest.mark.gpu
+def test_reference_unit_suite_unchanged_on_gpu():
+    """proj/tests/test_{service_dist,binning,analytics,simulator,workload,
+    experiment}.cpp, unchanged, against the drop-in: every test case passes."""
+    r = subprocess.run([_suite("unit_tests_b200")], capture_output=True, text=True, timeout=900)
+    print(r.stdout[-6000:])
+    assert r.returncode == 0, r.stdout[-6000:]
+    assert "All tests passed" in r.stdout

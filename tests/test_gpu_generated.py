@@ -75,6 +75,40 @@ def test_c4_symmetric_errors(pe):
     assert within_3se(p.latency_mean, p.latency_std, 2000, lat)
 
 
+C4_PE = [0.0, 0.05, 0.10, 0.15, 0.20, 0.25, 0.30]
+
+
+@pytest.mark.parametrize("k", [4, 8])
+@pytest.mark.parametrize("overload", [False, True], ids=["lam0.9cap", "overload"])
+def test_c4_full_grid_3se_and_monotone(k, overload):
+    """BASELINE configs[3]: k in {4, 8}, B=32, U[1,20], symmetric p_e 0..0.30,
+    at 0.9 x capacity and at overload.  Every point within 3 SE of the
+    reference's own replications; with common random numbers across p_e
+    (the error stream is separate, binning.hpp:239-240) overload throughput
+    is non-increasing and finite-rate latency non-decreasing in p_e."""
+    lam = math.inf if overload else 0.9 * bb.throughput(32, k, 1.0, 20.0)
+    n = 100_000
+    base = template(arrival_rate=lam, n_requests=n, batch_size=32, bins=bb.BinRule(k=k))
+    reps = 2000
+    pts = bb.run_experiment(bb.ExperimentSpec(base=base, axes=[bb.SweepAxis("p_e", C4_PE)],
+                                              replications=reps, seed=4))
+    assert [p.p_error for p in pts] == C4_PE
+    edges = bb.uniform_boundaries(k, 1.0, 20.0).edges
+    for p in pts:
+        thr, lat = ref_stats(dict(arrival_rate=lam, n_requests=n, batch_size=32, edges=edges,
+                                  lo=1.0, hi=20.0, error="symmetric", p_error=p.p_error), 32)
+        assert within_3se(p.throughput_mean, p.throughput_std, reps, thr), p
+        assert within_3se(p.latency_mean, p.latency_std, reps, lat), p
+    for a, b in zip(pts, pts[1:]):
+        if overload:
+            assert b.throughput_mean <= a.throughput_mean, (a.p_error, b.p_error)
+        else:
+            assert b.latency_mean >= a.latency_mean, (a.p_error, b.p_error)
+    if overload:  # p_e = 0 reproduces Theorem 1 (2%)
+        pred = bb.throughput(32, k, 1.0, 20.0)
+        assert abs(pts[0].throughput_mean - pred) / pred < 0.02
+
+
 def test_c5_lognormal_overload():
     t = template(arrival_rate=bb.kOverload, n_requests=100_000, batch_size=64,
                  bins=bb.BinRule(k=16), service=bb.ServiceSpec("lognormal", mu=0.0, sigma=1.0))

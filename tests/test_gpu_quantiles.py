@@ -81,6 +81,28 @@ def replica_streams(master, r, n, lam, lo, hi, errors):
     return arrivals, services, u_err
 
 
+def replica_streams_t(t, master, r, errors):
+    """The same, with the services from the engine's own sampler for any
+    service kind (bb_service_of_keys: the fused kernel's svc_of_key_t)."""
+    n, lam = t.n_requests, t.arrival_rate
+    sw = splitmix64(bb.replication_seed(master, r))
+    c2, c3 = sw & 0xFFFFFFFF, sw >> 32
+    i = np.arange(n, dtype=np.uint64)
+    rx, ry, rz, rw = philox_np(i, 0, c2, c3)
+    xg, xs = bits53(rx, ry), bits53(rz, rw)
+    if math.isinf(lam):
+        arrivals = np.zeros(n)
+    else:
+        arrivals = np.cumsum(bb.exponential_variates(xg, table=True) * (1.0 / lam))
+    services = bb.service_of_keys(t, xs)
+    u_err = None
+    if errors:
+        ex, ey, ez, ew = philox_np(i >> np.uint64(1), 1, c2, c3)
+        xe = np.where(i & np.uint64(1), bits53(ez, ew), bits53(ex, ey))
+        u_err = xe.astype(np.float64) * 2.0**-53
+    return arrivals, services, u_err
+
+
 def kernel_rep_metrics(t, reps, master):
     rep = torch.zeros(6 * reps, dtype=torch.float64, device="cuda")
     bb.points_shard_device([t], reps, master, 0, reps, rep.data_ptr())
@@ -208,3 +230,60 @@ def test_randomized_configs_bit_exact():
             assert got[0, r] == pytest.approx(m["throughput"], rel=1e-12), ctx
             assert got[2, r] == m["latency_p50"], ctx
             assert got[3, r] == m["latency_p99"], ctx
+
+
+def _cap_linear(B, k, a=0.5, b=0.03, lo=1.0, hi=1024.0):
+    return bb.throughput(B, k, a + b * lo, a + b * hi)
+
+
+SVC_CASES = [
+    # (label, service spec, lambda, n, B, k, flush, p_error, reps checked)
+    # C3 (BASELINE configs[2]): the benchmarked linear kind at the k=16/B=32 corner
+    ("c3_linear_k16_b32", bb.ServiceSpec("linear", 1.0, 1024.0, intercept=0.5, slope=0.03),
+     0.9 * _cap_linear(32, 16), 100000, 32, 16, True, 0.0, (0, 33)),
+    ("c3_linear_k1_b8_099", bb.ServiceSpec("linear", 1.0, 1024.0, intercept=0.5, slope=0.03),
+     0.99 * _cap_linear(8, 1), 100000, 8, 1, True, 0.0, (0, 5)),
+    ("linear_errors", bb.ServiceSpec("linear", 1.0, 1024.0, intercept=0.5, slope=0.03),
+     0.7 * _cap_linear(16, 8), 30000, 16, 8, True, 0.2, (1, 2)),
+    ("exponential_k4", bb.ServiceSpec("exponential", rate=0.1), 0.6 * 16 * 0.1 / 2.0,
+     40000, 16, 4, True, 0.0, (0, 7)),
+    ("exponential_noflush", bb.ServiceSpec("exponential", rate=1.0), 3.0, 20000, 8, 3, False,
+     0.1, (3,)),
+    # C5 shape (BASELINE configs[4]): log-normal, k=16, B=64, 10^6-request replications
+    ("c5_lognormal_k16_b64", bb.ServiceSpec("lognormal", mu=0.0, sigma=1.0), None,
+     1000000, 64, 16, True, 0.0, (0, 1)),
+    ("lognormal_overload", bb.ServiceSpec("lognormal", mu=0.0, sigma=1.0), math.inf,
+     50000, 64, 16, False, 0.0, (0, 2)),
+]
+
+
+@pytest.mark.parametrize("case", SVC_CASES, ids=[c[0] for c in SVC_CASES])
+def test_replication_quantiles_bit_exact_service_kinds(case):
+    """p50/p99 bit-exact vs the oracle for the linear (benchmarked), exponential
+    and log-normal service kinds, incl. the C3 and C5 corner shapes."""
+    _, svc, lam, n, B, k, flush, pe, check = case
+    if lam is None:  # 0.9 x the capacity of a pilot overload run (SURVEY 8(d) C5)
+        pilot = bb.run_point(bb.RunTemplate(n_requests=100_000, batch_size=B, bins=bb.BinRule(k=k),
+                                            service=svc, flush_partial=False), 7, 64)
+        lam = 0.9 * pilot.throughput_mean
+    kw = dict(arrival_rate=lam, n_requests=n, batch_size=B, flush_partial=flush,
+              bins=bb.BinRule(k=k), service=svc)
+    if pe > 0:
+        kw["error"] = bb.ErrorSpec("symmetric", pe)
+    t = bb.RunTemplate(**kw)
+    master = 20241205
+    reps = max(check) + 1
+    got = kernel_rep_metrics(t, reps, master)
+    edges = bb.template_edges(t)
+    for r in check:
+        a, s, u = replica_streams_t(t, master, r, pe > 0 and k > 1)
+        cfg = dict(arrival_rate=lam, n_requests=n, batch_size=B, flush_partial=flush,
+                   edges=edges, service="arrays", error="symmetric" if pe > 0 else "perfect",
+                   p_error=pe)
+        m, _ = O.run(O.oracle(), cfg, inputs=dict(arrivals=a, services=s, u_err=u), detail=False)
+        assert m["n_completed"] > 0
+        assert got[0, r] == pytest.approx(m["throughput"], rel=1e-12), (r, got[:, r], m)
+        assert got[4, r] == m["makespan"], (r, got[4, r], m["makespan"])
+        assert got[2, r] == m["latency_p50"], (r, got[2, r], m["latency_p50"])
+        assert got[3, r] == m["latency_p99"], (r, got[3, r], m["latency_p99"])
+        assert got[1, r] == pytest.approx(m["latency_mean"], rel=1e-9)
