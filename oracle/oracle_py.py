@@ -101,6 +101,7 @@ def _load(path, prefix):
         lib.bbo_generate_arrivals.argtypes = [C.c_uint64, C.c_double, C.c_uint64, _dp]
     else:
         run.argtypes = [C.POINTER(Cfg), C.POINTER(Metrics), C.POINTER(Detail)]
+        lib.bbref_run_arrays.argtypes = [C.POINTER(Cfg), _dp, _dp, C.POINTER(Metrics), C.POINTER(Detail)]
         lib.bbref_run_replicas.argtypes = [C.POINTER(Cfg), C.c_uint64, C.c_uint64, C.c_uint64,
                                            C.c_int, C.POINTER(Metrics), C.POINTER(C.c_double)]
         for f in ("bbref_throughput",):
@@ -213,6 +214,13 @@ def run(lib, d: dict, inputs: dict | None = None, detail: bool = True):
                 keep.pred = np.ascontiguousarray(inputs["pred_bin"], dtype=np.uint8)
                 inp.pred_bin = _ptr(keep.pred, _u8p)
         st = lib.run_fn(C.byref(c), C.byref(inp), C.byref(m), C.byref(det) if det else None)
+    elif inputs:  # the reference engine on given arrivals/services (bbref_run_arrays)
+        if inputs.get("u_err") is not None or inputs.get("pred_bin") is not None:
+            raise ValueError("reference arrays mode draws predictions from the seed's stream 2")
+        keep.a = np.ascontiguousarray(inputs["arrivals"], dtype=np.float64)
+        keep.s = np.ascontiguousarray(inputs["services"], dtype=np.float64)
+        st = lib.bbref_run_arrays(C.byref(c), _ptr(keep.a, _dp), _ptr(keep.s, _dp), C.byref(m),
+                                  C.byref(det) if det else None)
     else:
         st = lib.run_fn(C.byref(c), C.byref(m), C.byref(det) if det else None)
     if st != OK:

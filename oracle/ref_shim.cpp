@@ -14,17 +14,44 @@
 // tokens->time service and a log-normal service) are injected
 // through the reference's own detail::Engine(cfg, sampler) hook
 // (simulator.hpp:120-126), drawing from the reference's service stream.
+#include <algorithm>
 #include <atomic>
+#include <cctype>
 #include <chrono>
 #include <cmath>
+#include <cstddef>
+#include <cstdint>
+#include <cstdio>
 #include <cstring>
+#include <deque>
 #include <exception>
+#include <fstream>
+#include <functional>
+#include <json.hpp>
+#include <limits>
+#include <map>
 #include <mutex>
+#include <numeric>
+#include <optional>
+#include <ostream>
+#include <queue>
+#include <random>
+#include <sstream>
+#include <stdexcept>
 #include <string>
 #include <thread>
+#include <variant>
 #include <vector>
 
+// Given arrival arrays (bbref_run_arrays, below) need the engine's own event
+// loop with the arrivals scheduled from the array instead of its Poisson
+// stream.  detail::Engine keeps schedule() and its handlers private, so the
+// reference headers are read with private access opened (every standard and
+// JSON header they use is included above, unaffected).  Nothing in the
+// engine is changed: the same handlers run in the same event order.
+#define private public
 #include "binbatch/binbatch.hpp"
+#undef private
 #include "bb_oracle.h"
 
 using namespace binbatch;
@@ -295,6 +322,44 @@ int bbref_run_point(const bbo_config* c, uint64_t k, uint64_t master, uint64_t r
                         r.latency_p50, r.latency_p99, r.makespan_mean, r.busy_fraction_mean,
                         r.analytic_throughput, r.analytic_latency, r.analytic_max_throughput};
     std::memcpy(out, v, sizeof v);
+    return BBO_OK;
+  } catch (...) {
+    return code_of(std::current_exception());
+  }
+}
+
+// The reference engine on GIVEN arrival times and service times
+// (non-decreasing arrivals, e.g. quantised ones with tie groups of any size):
+// Engine::run (simulator.hpp:128-150) with schedule_arrivals (:174-185)
+// replaced by scheduling arrival i at arrivals[i]; services come through the
+// engine's sampler hook (:120-126); predicted bins from the error model on
+// the seed's stream 2, exactly as in a generated run.
+int bbref_run_arrays(const bbo_config* c, const double* arrivals, const double* services,
+                     bbo_metrics* m, bbo_detail* d) {
+  try {
+    SimConfig cfg = to_sim(c);
+    detail::Engine e(cfg, [services](std::size_t id, RandomStream&) { return services[id]; });
+    e.validate();
+    const std::size_t k = e.cfg_.bins.bin_count();
+    e.bin_queues_.assign(k + 1, {});
+    e.batch_counts_.assign(k, 0);
+    e.requests_.reserve(cfg.n_requests);
+    e.idle_servers_ = cfg.n_servers;
+    for (std::size_t i = 0; i < cfg.n_requests; ++i) e.schedule(arrivals[i], detail::EventKind::arrival, i);
+    while (!e.events_.empty()) {
+      const detail::Event ev = e.events_.top();
+      e.events_.pop();
+      e.now_ = ev.time;
+      switch (ev.kind) {
+        case detail::EventKind::batch_done: e.on_batch_done(ev.a); break;
+        case detail::EventKind::arrival: e.on_arrival(ev.a); break;
+        case detail::EventKind::formation: e.on_formation(ev.a); break;
+        case detail::EventKind::flush_timer: e.on_flush_timer(ev.a, ev.b); break;
+        case detail::EventKind::drain_bin: e.on_drain(ev.a); break;
+      }
+    }
+    const SimResult r = e.finish();
+    fill(r, k, m, d);
     return BBO_OK;
   } catch (...) {
     return code_of(std::current_exception());

@@ -528,6 +528,9 @@ __global__ void __launch_bounds__(kGenThreads, Q ? 2 : BB_GEN_MINB) gen_kernel(c
         double leftover = 0.0;
         // without flush the open batches still form when their timers fire
         if (TM && !failed && !flush) fire_until(CUDART_INF);
+        // with flush, a timer due exactly at the last arrival was armed before
+        // the drains were scheduled (lower seq): it fires first (:203-205)
+        if (TM && !failed && flush) fire_until(__longlong_as_double(__double_as_longlong(R.t) + 1));
         if (!failed) {
           for (uint32_t b = 0; b < k; ++b) {
             const uint64_t s0 = st[b * 32 + lane];
@@ -734,13 +737,19 @@ __global__ void __launch_bounds__(kGenThreads, Q ? 2 : BB_GEN_MINB) gen_kernel(c
             latw = R.latw;
             mk = R.D;
           } else if (Q) {  // one server: completions are the running sum in dispatch order
-            double D = 0.0;
+            // (the makespan and busy sum are the reference's dispatch-order
+            // sums, simulator.hpp:261-263, not the closing-order ones above)
+            double D = 0.0, bsum = 0.0;
             for (uint32_t x = 0; x < nbt; ++x) {
-              D = __dadd_rn(x < nb0 ? D : fmax(D, P.max_batch_wait), ovS[(size_t)x * gstride]);
+              const double S = ovS[(size_t)x * gstride];
+              D = __dadd_rn(x < nb0 ? D : fmax(D, P.max_batch_wait), S);
+              bsum = __dadd_rn(bsum, S);
               ovS[(size_t)x * gstride] = D;
               q_lmin = fmin(q_lmin, D);
               q_lmax = fmax(q_lmax, D);
             }
+            mk = D;
+            busy = bsum;
           }
           if (nc > 0) {
             mk_out = mk;

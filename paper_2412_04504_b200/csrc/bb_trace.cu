@@ -587,6 +587,143 @@ __global__ void order_kernel(WS ws, uint32_t* map, uint32_t* order, uint32_t* df
   dfirst[pos] = (uint32_t)before;
 }
 
+// ------------------------------------------------ general tie groups (path 2)
+// A maximal group G = [s, e) of equal arrival times t.
+// Every bin enters G with fewer than B queued, all of G's arrivals (rank 1)
+// are processed before any formation at t (rank 2), and a bin schedules one
+// formation, at its closing request c_b (queue.size() == B,
+// simulator.hpp:196-199).  on_formation re-schedules itself at the back while
+// the bin still holds >= B (:208-216), so the batches formed at t go out in
+// rounds: round j holds every bin with more than j batches in G, in c_b
+// order.  In the final group with flush the drains (scheduled after round 0's
+// formations, :202-205) take, bin by bin, the remaining full batches and then
+// the partial (:218-221); the re-scheduled formations then find < B.
+// A group of at most B arrivals forms at most one batch per bin, in closing
+// order: the fast path's identity.  So only groups of more than B arrivals
+// are re-ordered here, each inside its own range of closing records.
+
+// groups of more than B equal arrivals: (start, end) pairs, any order
+__global__ void tie_groups_kernel(const double* __restrict__ a, uint32_t n, uint32_t B, uint2* groups,
+                                  uint32_t* ngroups) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const double v = a[i];
+    if (i > 0 && a[i - 1] == v) continue;
+    if ((uint64_t)i + B >= n || a[i + B] != v) continue;
+    uint32_t lo = i + B + 1, hi = n;  // first index past the group (a is non-decreasing)
+    while (lo < hi) {
+      const uint32_t mid = lo + (hi - lo) / 2;
+      if (a[mid] == v) lo = mid + 1;
+      else hi = mid;
+    }
+    groups[atomicAdd(ngroups, 1u)] = make_uint2(i, lo);
+  }
+}
+
+struct TieArgs {
+  const uint2* groups;
+  const uint32_t* ngroups;
+  const unsigned long long* desc1;  // partition look-back: inclusive per-tile bin counts
+  WS ws;
+  uint32_t *map, *order, *dfirst;
+  uint32_t n, k, B;
+  int32_t flush;
+};
+
+// One block per group: per-bin counts at its ends (tile prefix + the tile's
+// head), the round-robin / drain position of each of its records.
+__global__ void __launch_bounds__(256) tie_order_kernel(TieArgs T) {
+  __shared__ uint32_t s_c[2][32], s_F[32], s_j0[32], s_cf[32], s_rem[32];
+  __shared__ uint32_t s_fb[32], s_pc[32], s_pr[32];
+  __shared__ uint32_t s_qlo, s_qhi, s_Z;
+  const Info* I = T.ws.info;
+  const uint32_t tid = threadIdx.x, k = T.k, B = T.B;
+  for (uint32_t g = blockIdx.x; g < *T.ngroups; g += gridDim.x) {
+    const uint2 G = T.groups[g];
+    __syncthreads();
+    if (tid < 32) s_c[0][tid] = s_c[1][tid] = 0;
+    __syncthreads();
+    // count_b[0, x) = inclusive count of the previous tile + this tile's head
+#pragma unroll
+    for (int side = 0; side < 2; ++side) {
+      const uint32_t x = side ? G.y : G.x;
+      const uint32_t t = x / TILE;
+      if (tid < k && t > 0) atomicAdd(&s_c[side][tid], (uint32_t)(T.desc1[(uint64_t)(t - 1) * k + tid] & VAL_MASK));
+      for (uint32_t i = t * TILE + tid; i < x; i += blockDim.x) atomicAdd(&s_c[side][T.ws.pb8[i] - 1], 1u);
+    }
+    __syncthreads();
+    if (tid < 32) {
+      const uint32_t cs = tid < k ? s_c[0][tid] : 0, ce = tid < k ? s_c[1][tid] : 0;
+      const uint32_t js = cs / B, je = ce / B, F = je - js;
+      s_F[tid] = F;
+      s_j0[tid] = js;
+      s_cf[tid] = 0xFFFFFFFFu;
+      const uint32_t rem = (T.flush && G.y == T.n) ? ce - je * B : 0;  // the final partials
+      s_rem[tid] = rem;
+      uint32_t qlo = js, qhi = je, Z = F >= 1;
+      // drain bookkeeping: exclusive sums over lower bins
+      uint32_t fb = F ? F - 1 : 0, pc = rem != 0, pr = rem;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t a1 = __shfl_up_sync(0xffffffffu, fb, o), a2 = __shfl_up_sync(0xffffffffu, pc, o),
+                       a3 = __shfl_up_sync(0xffffffffu, pr, o);
+        if (tid >= o) fb += a1, pc += a2, pr += a3;
+      }
+      s_fb[tid] = fb - (F ? F - 1 : 0);
+      s_pc[tid] = pc - (rem != 0);
+      s_pr[tid] = pr - rem;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        qlo += __shfl_xor_sync(0xffffffffu, qlo, o);
+        qhi += __shfl_xor_sync(0xffffffffu, qhi, o);
+        Z += __shfl_xor_sync(0xffffffffu, Z, o);
+      }
+      if (tid == 0) s_qlo = qlo, s_qhi = qhi, s_Z = Z;
+    }
+    __syncthreads();
+    const uint32_t qlo = s_qlo, qhi = s_qhi;
+    // c_b: the closing request of bin b's first batch in G (its round-0 key)
+    for (uint32_t q = qlo + tid; q < qhi; q += blockDim.x) {
+      const uint32_t b = T.ws.recBin[q] - 1;
+      if (T.ws.recJ[q] == s_j0[b]) s_cf[b] = T.ws.recC[q];
+    }
+    __syncthreads();
+    const bool final_drain = T.flush && G.y == T.n;
+    const uint32_t qend = final_drain ? I->nb : qhi;
+    for (uint32_t x = qlo + tid; x < qend; x += blockDim.x) {
+      const uint32_t q = x < qhi ? x : I->nclose + (x - qhi);  // then the partial records
+      if (q >= I->nb) break;
+      const uint32_t b = T.ws.recBin[q] - 1, jg = T.ws.recJ[q], Fb = s_F[b];
+      uint32_t pos;
+      unsigned long long before;
+      if (x >= qhi) {  // on_drain's partial, after the bin's remaining full batches
+        const uint32_t f = s_fb[b] + (Fb ? Fb - 1 : 0);
+        pos = qlo + s_Z + f + s_pc[b];
+        before = (unsigned long long)B * (qlo + s_Z + f) + s_pr[b];
+      } else {
+        const uint32_t jr = jg - s_j0[b];
+        if (final_drain && jr >= 1) {  // on_drain: full batches in bin order
+          const uint32_t f = s_fb[b] + (jr - 1);
+          pos = qlo + s_Z + f + s_pc[b];
+          before = (unsigned long long)B * (qlo + s_Z + f) + s_pr[b];
+        } else {  // round jr, first-closing order
+          uint32_t p = 0;
+          const uint32_t cb = s_cf[b];
+          for (uint32_t b2 = 0; b2 < k; ++b2) {
+            const uint32_t F2 = s_F[b2];
+            if (!final_drain) p += F2 < jr ? F2 : jr;
+            p += (s_cf[b2] < cb) && (F2 > jr);
+          }
+          pos = qlo + p;
+          before = (unsigned long long)B * pos;
+        }
+      }
+      T.order[pos] = q;
+      T.map[I->bin_base[b] + jg] = pos;
+      T.dfirst[pos] = (uint32_t)before;
+    }
+  }
+}
+
 __global__ void gather_kernel(WS ws, const uint32_t* order, int32_t path, uint32_t B, double* dR,
                               double* dS, uint8_t* dBin, uint32_t* dSize) {
   const Info* I = ws.info;
@@ -1550,7 +1687,8 @@ struct TmArgs {
   uint32_t* recN;    // members
   uint8_t* recB;     // bin (0-based)
   unsigned long long* key1;  // formation time bits (~0: unused slot)
-  uint32_t* key2;            // event class << 8 | bin
+  unsigned long long* key2;  // event class << 32 | (timer: its front's request index
+                             //   = the arming order, the event seq; else the bin)
   uint32_t* segj;    // per list position
   uint32_t* nrec;    // per bin
 };
@@ -1570,7 +1708,7 @@ __global__ void __launch_bounds__(32) tm_segment_kernel(TmArgs T) {
       T.recN[q] = size;
       T.recB[q] = (uint8_t)b;
       T.key1[q] = (unsigned long long)__double_as_longlong(formed);
-      T.key2[q] = (cls << 8) | b;
+      T.key2[q] = ((unsigned long long)cls << 32) | (cls == TM_TIMER ? T.list[off + f] : b);
     }
     ++nseg;
     open = false;
@@ -1884,13 +2022,6 @@ void trace_run(const TraceArgs& A, TraceResult* R, cudaStream_t s) {
     snprintf(R->message, sizeof R->message, "trace arrays: arrivals must be non-decreasing");
     goto cleanup;
   }
-  if (info.path == 2) {
-    R->status = BB_EUNSUPPORTED;
-    snprintf(R->message, sizeof R->message,
-             "trace arrays: a tie group of more than B equal arrivals (other than a single "
-             "all-equal group) is not supported yet");
-    goto cleanup;
-  }
   R->path = (int32_t)info.path;
   // max_batch_wait: overload with flush drains every bin at t = 0, so the
   // timers go stale and the plain pipeline applies; otherwise the timer path
@@ -1964,7 +2095,8 @@ void trace_run(const TraceArgs& A, TraceResult* R, cudaStream_t s) {
         hoff[b] = acc;
         acc += hcnt[b];
       }
-      uint32_t *d_off, *d_cnt, *list, *segj, *nrec, *recP, *recN, *key2, *key2b, *val, *valb;
+      uint32_t *d_off, *d_cnt, *list, *segj, *nrec, *recP, *recN, *val, *valb;
+      unsigned long long *key2, *key2b;
       uint8_t* recB;
       unsigned long long *key1, *key1b;
       double *recF, *recS, a_last = 0;
@@ -1980,8 +2112,8 @@ void trace_run(const TraceArgs& A, TraceResult* R, cudaStream_t s) {
       BB_CK(pool.alloc((void**)&recS, (size_t)n * 8));
       BB_CK(pool.alloc((void**)&key1, (size_t)n * 8));
       BB_CK(pool.alloc((void**)&key1b, (size_t)n * 8));
-      BB_CK(pool.alloc((void**)&key2, (size_t)n * 4));
-      BB_CK(pool.alloc((void**)&key2b, (size_t)n * 4));
+      BB_CK(pool.alloc((void**)&key2, (size_t)n * 8));
+      BB_CK(pool.alloc((void**)&key2b, (size_t)n * 8));
       BB_CK(pool.alloc((void**)&val, (size_t)n * 4));
       BB_CK(pool.alloc((void**)&valb, (size_t)n * 4));
       BB_CK(cudaMemcpyAsync(d_off, hoff.data(), (size_t)k * 4, cudaMemcpyHostToDevice, s));
@@ -2005,21 +2137,22 @@ void trace_run(const TraceArgs& A, TraceResult* R, cudaStream_t s) {
         nb += hn[b];
         R->per_bin[b] = hn[b];
       }
-      // dispatch order: stable radix sorts, event class | bin first, then time
+      // dispatch order: stable radix sorts, (event class, arming order | bin) first, then time
       {
         std::vector<uint32_t> iota(n);
         for (uint32_t i = 0; i < n; ++i) iota[i] = i;
         BB_CK(cudaMemcpyAsync(val, iota.data(), (size_t)n * 4, cudaMemcpyHostToDevice, s));
-        cub::DoubleBuffer<uint32_t> k2(key2, key2b), v2(val, valb);
+        cub::DoubleBuffer<unsigned long long> k2(key2, key2b);
+        cub::DoubleBuffer<uint32_t> v2(val, valb);
         size_t tb1 = 0, tb2 = 0;
         void* tmp = nullptr;
-        BB_CK(cub::DeviceRadixSort::SortPairs(nullptr, tb1, k2, v2, (int)n, 0, 16, s));
+        BB_CK(cub::DeviceRadixSort::SortPairs(nullptr, tb1, k2, v2, (int)n, 0, 34, s));
         cub::DoubleBuffer<unsigned long long> k1(key1, key1b);
         BB_CK(cub::DeviceRadixSort::SortPairs(nullptr, tb2, k1, v2, (int)n, 0, 64, s));
         BB_CK(pool.alloc(&tmp, std::max(tb1, tb2)));
         // the time keys must follow the first sort's permutation: sort
         // (class|bin, (time, index)) then (time, index) -- gather time by index
-        BB_CK(cub::DeviceRadixSort::SortPairs(tmp, tb1, k2, v2, (int)n, 0, 16, s));
+        BB_CK(cub::DeviceRadixSort::SortPairs(tmp, tb1, k2, v2, (int)n, 0, 34, s));
         note_launch();
         uint32_t* perm = v2.Current();
         // key1 in the class|bin order
@@ -2081,10 +2214,30 @@ void trace_run(const TraceArgs& A, TraceResult* R, cudaStream_t s) {
       BB_CK(cudaGetLastError());
     }
     if (!tm) {
+      // path 2 (tie groups of more than B at finite times): closing order
+      // first, then each such group re-orders its own range of records
+      const int32_t opath = info.path == 2 ? 0 : (int32_t)info.path;
       if (nb) order_kernel<<<grid_for(nb, 256), 256, 0, s>>>(ws, map, order, dfirst, k, B, A.flush,
-                                                     (int32_t)info.path, (int32_t)tmo);
+                                                     opath, (int32_t)tmo);
       note_launch();
       BB_CK(cudaGetLastError());
+      if (info.path == 2 && nb) {
+        const uint32_t gcap = n / (B + 1) + 1;
+        uint2* groups;
+        uint32_t* ngroups;
+        BB_CK(pool.alloc((void**)&groups, (size_t)gcap * 8));
+        BB_CK(pool.alloc((void**)&ngroups, 4));
+        BB_CK(cudaMemsetAsync(ngroups, 0, 4, s));
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        tie_groups_kernel<<<std::min<uint32_t>(grid_for(n, 256), sms * 8), 256, 0, s>>>(A.a, n, B, groups,
+                                                                                      ngroups);
+        TieArgs T{groups, ngroups, ws.desc1, ws, map, order, dfirst, n, k, B, A.flush};
+        tie_order_kernel<<<std::min<uint32_t>(gcap, sms * 4), 256, 0, s>>>(T);
+        note_launch(2);
+        BB_CK(cudaGetLastError());
+      }
       if (nb) gather_kernel<<<grid_for(nb, 256), 256, 0, s>>>(ws, order, (int32_t)info.path, B, dR, dS,
                                                       A.bat_bin, A.bat_size);
       note_launch();

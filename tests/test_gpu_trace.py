@@ -143,18 +143,59 @@ def test_small_tie_groups_use_fast_path_exactly():
     rng = np.random.default_rng(5)
     n, B, k = 20000, 16, 4
     a = np.floor(np.cumsum(rng.exponential(1 / 3.0, n)) * 4) / 4  # many ties
-    g = np.diff(np.r_[-1.0, a]) == 0
-    run = np.max(np.diff(np.flatnonzero(np.r_[True, ~g[1:], True]))) if n else 0
-    assume = run <= B
     s = rng.uniform(1.0, 20.0, n)
     edges = bb.uniform_boundaries(k, 1.0, 20.0).edges
     cfg = dict(arrival_rate=3.0, n_requests=n, batch_size=B, edges=edges, seed=0, service="arrays")
     m, d = O.run(O.oracle(), cfg, dict(arrivals=a, services=s))
-    exp = {key: d[key] for key in d}
-    if not assume:
-        pytest.skip("generated a tie group larger than B")
     res = bb.run_trace(sim_config(cfg), a, s, detailed=True)
-    check_against(res, exp, n)
+    check_against(res, {key: d[key] for key in d}, n)
+
+
+def _tie_case(seed):
+    """given arrivals with tie groups of more than B equal times at finite
+    times (App. A.2 rules 1-3), incl. a final group larger than B"""
+    rng = np.random.default_rng(77 + seed)
+    r = random.Random(seed)
+    k = r.choice([1, 2, 3, 4, 8, 16])
+    B = r.choice([1, 2, 4, 8, 16])
+    n = r.randint(2000, 40000)
+    a = np.floor(np.cumsum(rng.exponential(1.0 / r.uniform(0.5, 4.0), n)) / r.choice([1.0, 4.0, 16.0]))
+    for _ in range(r.randint(1, 6)):
+        i = int(rng.integers(0, n - 1))
+        a[i:i + r.randint(B + 1, 8 * B + 3)] = a[i]
+    if r.random() < 0.4:
+        a[-r.randint(B + 1, 6 * B + 1):] = a[-1]
+    a = np.maximum.accumulate(a)
+    s = rng.uniform(1.0, 20.0, n)
+    cfg = dict(arrival_rate=2.0, n_requests=n, batch_size=B, seed=r.getrandbits(64),
+               edges=bb.uniform_boundaries(k, 1.0, 20.0).edges, service="arrays",
+               flush_partial=r.random() < 0.6, n_servers=r.choice([1, 1, 1, 3]))
+    if r.random() < 0.5:
+        cfg.update(error="symmetric", p_error=r.choice([0.1, 0.4]))
+    return cfg, a, s
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_large_tie_groups_bit_exact(seed):
+    """Tie groups larger than B at finite times: round-robin formations in
+    first-closing order, drains in bin order in the final group -- bit-exact
+    against the reference's own event loop on the same arrays (bbref_run_arrays;
+    the C restatement where the reference shim is not built)."""
+    cfg, a, s = _tie_case(seed)
+    n = cfg["n_requests"]
+    g = np.diff(np.flatnonzero(np.r_[True, np.diff(a) != 0, True]))
+    assert g.max() > cfg["batch_size"]  # the case exercises the general path
+    draws = cfg.get("error") == "symmetric" and len(cfg["edges"]) > 2
+    u = O.stream_uniform01(O.oracle(), cfg["seed"], 2, n) if draws else None
+    lib = O.reference() if O.have_reference() else O.oracle()
+    m, d = O.run(lib, cfg, dict(arrivals=a, services=s) if lib is O.reference()
+                 else dict(arrivals=a, services=s, u_err=u))
+    c = sim_config(cfg)
+    c.n_servers = cfg["n_servers"]
+    res = bb.run_trace(c, a, s, u_err=u, detailed=True)
+    check_against(res, {key: d[key] for key in d}, n)
+    lat = d["req_completion"] - d["req_arrival"]
+    check_metrics(res.metrics, m, n, np.nansum(np.abs(lat)), d["bat_service"].sum())
 
 
 def test_errors_have_reference_categories():

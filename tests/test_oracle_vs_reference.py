@@ -70,3 +70,43 @@ def test_oracle_equals_reference(seed):
     for key in ("throughput", "makespan", "latency_mean", "latency_p50", "latency_p99",
                 "server_busy_fraction", "n_completed", "n_batches"):
         assert same_bits(mo[key], mr[key]), key
+
+
+def tied_arrivals(rng: np.random.Generator, n, rate, quantum, bursts=0, burst_len=0):
+    """non-decreasing arrivals with tie groups: Poisson times rounded down to a
+    quantum, plus `bursts` runs of `burst_len` equal times (groups > B)"""
+    a = np.floor(np.cumsum(rng.exponential(1.0 / rate, n)) / quantum) * quantum
+    for _ in range(bursts):
+        i = int(rng.integers(0, max(1, n - burst_len)))
+        a[i:i + burst_len] = a[i]
+    return np.maximum.accumulate(a)
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_oracle_equals_reference_on_tie_groups(seed):
+    """Given arrival arrays with tie groups of any size (App. A.2): the C
+    restatement against the reference's own event loop (bbref_run_arrays)."""
+    rng = np.random.default_rng(1000 + seed)
+    r = random.Random(seed)
+    k = r.choice([1, 2, 3, 4, 8])
+    B = r.choice([1, 2, 3, 4, 8, 16])
+    n = r.randint(max(B, 50), 4000)
+    a = tied_arrivals(rng, n, r.uniform(0.5, 4.0), r.choice([0.25, 1.0, 4.0, 16.0]),
+                      bursts=r.randint(0, 3), burst_len=r.randint(B + 1, 6 * B + 2))
+    if r.random() < 0.2:
+        a[-r.randint(B + 1, 5 * B + 1):] = a[-1]  # a final group larger than B
+    s = rng.uniform(1.0, 20.0, n)
+    cfg = dict(arrival_rate=2.0, n_requests=n, batch_size=B, seed=r.getrandbits(64),
+               edges=O.uniform_boundaries(k, 1.0, 20.0).tolist(), service="arrays",
+               flush_partial=r.random() < 0.6, n_servers=r.choice([1, 1, 2, 5]))
+    if r.random() < 0.5:
+        cfg.update(error="symmetric", p_error=r.choice([0.1, 0.4]))
+    draws = cfg.get("error") == "symmetric" and k > 1
+    u = O.stream_uniform01(O.oracle(), cfg["seed"], 2, n) if draws else None
+    mr, dr = O.run(O.reference(), cfg, dict(arrivals=a, services=s))
+    mo, do = O.run(O.oracle(), cfg, dict(arrivals=a, services=s, u_err=u))
+    for key in REQ_KEYS + BAT_KEYS:
+        assert same_bits(do[key], dr[key]), key
+    for key in ("makespan", "throughput", "latency_mean", "latency_p50", "latency_p99",
+                "server_busy_fraction", "n_completed"):
+        assert same_bits(mo[key], mr[key]), key
