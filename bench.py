@@ -13,8 +13,9 @@ replications, per-point mean/std), fused generated-mode kernel (Philox).
 N>1: launched by torch.distributed.run, one rank per GPU over NCCL.  Weak
 scaling: every rank simulates R replications of every point
 (replications [rank*R, (rank+1)*R) of an N*R-replication sweep, seeds
-replication_seed(seed, r)); the per-replication metrics are combined with ONE
-NCCL all-reduce and reduced per point exactly as run_point does.
+replication_seed(seed, r)) into its own block; the blocks are combined with
+ONE NCCL all-gather and reduced per point in replication order exactly as
+run_point does.
 
 --impl reference: the unmodified reference engine (oracle/_ref/libbbref.so,
 compiled from /root/reference's headers) on all host cores over a bounded
@@ -210,7 +211,7 @@ def workload_config(args, reps):
                       "run_point does (experiment.hpp:256-279)"),
         "l2": "no HBM-resident inputs in generated mode; a 512 MiB buffer is written between "
               "timed steps anyway (L2 flushed)",
-        "parallelism": f"replicas sharded over {args.gpus} GPU(s), 1 NCCL all-reduce per step",
+        "parallelism": f"replicas sharded over {args.gpus} GPU(s), 1 NCCL all-gather per step",
     }
 
 
@@ -263,7 +264,8 @@ def main():
                                                  slope=B_SLOPE)) for p in pts]
     P, R = len(tpl), args.reps
     Rtot = R * world
-    rep = torch.zeros(6 * P * Rtot, dtype=torch.float64, device=dev)
+    block = torch.empty(6 * P * R, dtype=torch.float64, device=dev)  # this rank's replications
+    gathered = torch.empty(6 * P * Rtot, dtype=torch.float64, device=dev) if world > 1 else block
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
     results = {}
 
@@ -272,10 +274,9 @@ def main():
     lo, hi = bbdist.weak_shard(R, rank)
 
     def step():
-        rep.zero_()
-        bb.points_shard_device(tpl, Rtot, SEED, lo, hi, rep.data_ptr(), sptr)
-        bbdist.combine(rep)  # the sweep's one NCCL all-reduce (no-op at N=1)
-        results["pts"] = bb.points_reduce_device(tpl, Rtot, rep.data_ptr(), sptr)
+        bb.points_shard_local_device(tpl, Rtot, SEED, lo, hi, block.data_ptr(), sptr)
+        bbdist.gather(block, gathered)  # the sweep's one NCCL all-gather (no-op at N=1)
+        results["pts"] = bb.points_reduce_gathered_device(tpl, Rtot, world, gathered.data_ptr(), sptr)
 
     for _ in range(args.warmup):
         step()
@@ -331,7 +332,7 @@ def main():
     e2e = {"value": requests_step * n_e2e / e2e_s, "unit": "requests/s",
            "h2d_bytes_per_step": int(h2d // n_e2e), "d2h_bytes_per_step": int(d2h // n_e2e),
            "api": "bb_run_points (host templates -> host PointResults)" if world == 1
-           else "host spec -> shard -> NCCL all-reduce -> reduce -> host PointResults"}
+           else "host spec -> shard -> NCCL all-gather -> reduce -> host PointResults"}
     # consistency: the e2e results equal the device-timed results
     same = all(a.throughput_mean == b.throughput_mean for a, b in zip(out, results["pts"]))
 

@@ -260,7 +260,9 @@ bb_status bb_run_experiment(const bb_experiment_spec* spec, unsigned jobs, bb_po
  * simulate replications [rep_begin, rep_end) of every point of `spec` on the
  * current device into the device array `rep_metrics_dev`
  * ([BB_REP_FIELDS][n_points*replications] doubles, replica-major within a
- * point; entries outside the shard are left untouched).  Stream-ordered. */
+ * point; entries outside the shard are left untouched).  Stream-ordered (no
+ * host synchronisation): a device-side error (a service outside the bin
+ * support) is reported by the next *_reduce_device call on the device. */
 bb_status bb_sweep_shard_device(const bb_experiment_spec* spec, uint64_t rep_begin,
                                 uint64_t rep_end, double* rep_metrics_dev, void* stream);
 /* The same for an explicit list of sweep points (points whose parameters do
@@ -275,6 +277,28 @@ bb_status bb_run_points(const bb_run_template* points, uint64_t n_points, uint64
 bb_status bb_points_reduce_device(const bb_run_template* points, uint64_t n_points,
                                   uint64_t replications, const double* rep_metrics_dev,
                                   bb_point_result* out, void* stream);
+/* One process per GPU, gather instead of all-reduce: shard
+ * [rep_begin, rep_end) written as its own block [BB_REP_FIELDS][n_points]
+ * [rep_end - rep_begin] (no zero padding); the blocks of shards
+ * [R c / C, R (c+1) / C), c = 0..C-1, concatenated in shard order (an
+ * all-gather) are reduced by bb_points_reduce_gathered_device in replication
+ * order, bit-identical to a single-device run.  Stream-ordered: a device-side
+ * error is reported by the next reduce on the same device. */
+bb_status bb_points_shard_local_device(const bb_run_template* points, uint64_t n_points,
+                                       uint64_t replications, uint64_t seed, uint64_t rep_begin,
+                                       uint64_t rep_end, double* shard_dev, void* stream);
+bb_status bb_points_reduce_gathered_device(const bb_run_template* points, uint64_t n_points,
+                                           uint64_t replications, uint32_t n_shards,
+                                           const double* gathered_dev, bb_point_result* out,
+                                           void* stream);
+/* Devices the host-side sweeps (bb_run_experiment / bb_run_points /
+ * bb_run_point, Philox streams) spread their replications over in this
+ * process: one host thread per entry, results gathered on devices[0] by peer
+ * stores and reduced there (the reference's std::thread pool over points,
+ * experiment.hpp:342-368, as a pool over GPUs).  Entries may repeat (shards
+ * on one device run on separate streams); n = 0 restores the default, the
+ * calling thread's current device.  Results never depend on the list. */
+bb_status bb_set_devices(const int32_t* devices, uint32_t n);
 /* Per-point aggregation of a complete rep_metrics array (mean_std,
  * experiment.hpp:188-200 + run_point :266-306); blocks until `out` is filled. */
 bb_status bb_sweep_reduce_device(const bb_experiment_spec* spec, const double* rep_metrics_dev,

@@ -1036,6 +1036,14 @@ inline PointResult run_point(const RunTemplate& t, std::uint64_t master_seed, st
   return run_point(t, resolve_workload(t), master_seed, replications, rng);
 }
 
+// GPUs the sweeps below spread their replications over in this process (one
+// host thread per device, results gathered on devices[0]; repeats allowed);
+// empty: the current device.  Results never depend on the list.
+inline void set_devices(const std::vector<int>& devices) {
+  std::vector<int32_t> d(devices.begin(), devices.end());
+  detail::check(bb_set_devices(d.empty() ? nullptr : d.data(), static_cast<uint32_t>(d.size())));
+}
+
 // run_experiment (experiment.hpp:312-370): every point x replication in one
 // device launch; `jobs` is accepted and never changes results.  A failing
 // point throws std::runtime_error("experiment '<name>': sweep point <i> failed: ...").

@@ -659,6 +659,36 @@ def points_reduce_device(points: Sequence[RunTemplate], replications: int, rep_p
     return [_point(out[i]) for i in range(len(points))]
 
 
+def points_shard_local_device(points: Sequence[RunTemplate], replications: int, seed: int,
+                              rep_begin: int, rep_end: int, shard_ptr: int, stream: int = 0) -> None:
+    """Shard [rep_begin, rep_end) into its own block [6][points][rep_end-rep_begin]
+    (what an all-gather of the ranks' blocks concatenates)."""
+    arr, keep = _points_array(points)
+    _check(_lib.bb_points_shard_local_device(arr, len(points), int(replications),
+                                             int(seed) & (2**64 - 1), rep_begin, rep_end,
+                                             C.c_void_p(shard_ptr), C.c_void_p(stream) if stream else None))
+
+
+def points_reduce_gathered_device(points: Sequence[RunTemplate], replications: int, n_shards: int,
+                                  gathered_ptr: int, stream: int = 0) -> List[PointResult]:
+    """run_point's per-point reduction over the concatenated blocks of n_shards
+    shards [R c / C, R (c+1) / C) (replication order, bit-identical to one device)."""
+    arr, keep = _points_array(points)
+    out = (_capi.PointResultC * len(points))()
+    _check(_lib.bb_points_reduce_gathered_device(arr, len(points), int(replications), int(n_shards),
+                                                 C.c_void_p(gathered_ptr), out,
+                                                 C.c_void_p(stream) if stream else None))
+    return [_point(out[i]) for i in range(len(points))]
+
+
+def set_devices(devices: Sequence[int] = ()) -> None:
+    """Devices host-side sweeps (run_experiment / run_points / run_point) spread
+    their replications over: one host thread per entry, gathered on devices[0].
+    Entries may repeat; () restores the current device."""
+    arr = (C.c_int32 * max(1, len(devices)))(*[int(d) for d in devices])
+    _check(_lib.bb_set_devices(arr, len(devices)))
+
+
 def replication_seed(master: int, rep: int) -> int:
     """experiment.hpp:90-92"""
     return int(_lib.bb_replication_seed(master & (2**64 - 1), rep & (2**64 - 1)))

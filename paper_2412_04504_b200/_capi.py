@@ -117,6 +117,7 @@ EXPORTS = [
     "bb_service_of_keys", "bb_expected_service_time", "bb_throughput", "bb_max_throughput",
     "bb_min_bins_for_throughput", "bb_expected_latency", "bb_exponential_service_bound",
     "bb_harmonic_number", "bb_assign_bin", "bb_brute_force_boundaries",
+    "bb_points_shard_local_device", "bb_points_reduce_gathered_device", "bb_set_devices",
 ]
 
 
@@ -154,6 +155,12 @@ def load():
                                   P(PointResultC)]
     lib.bb_points_reduce_device.argtypes = [P(RunTemplateC), C.c_uint64, C.c_uint64, C.c_void_p,
                                             P(PointResultC), C.c_void_p]
+    lib.bb_points_shard_local_device.argtypes = [P(RunTemplateC), C.c_uint64, C.c_uint64, C.c_uint64,
+                                                 C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p]
+    lib.bb_points_reduce_gathered_device.argtypes = [P(RunTemplateC), C.c_uint64, C.c_uint64,
+                                                     C.c_uint32, C.c_void_p, P(PointResultC),
+                                                     C.c_void_p]
+    lib.bb_set_devices.argtypes = [P(C.c_int32), C.c_uint32]
     lib.bb_experiment_points.argtypes = [P(ExperimentSpecC), P(C.c_uint64)]
     lib.bb_uniform_boundaries.argtypes = [C.c_uint64, C.c_double, C.c_double, _dp]
     lib.bb_exponential_boundaries.argtypes = [C.c_uint64, C.c_double, C.c_uint64, _dp]

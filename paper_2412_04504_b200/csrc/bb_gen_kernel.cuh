@@ -248,7 +248,8 @@ __global__ void __launch_bounds__(kGenThreads, Q ? 2 : BB_GEN_MINB) gen_kernel(c
   const uint32_t nrep = L.rep_end - L.rep_begin;
   const uint32_t chunks = (nrep + 31) / 32;
   const uint64_t n_items = (uint64_t)chunks * L.n_points;
-  const uint64_t stride = (uint64_t)L.points_total * L.reps_total;
+  const uint32_t out_reps = L.out_reps ? L.out_reps : L.reps_total;
+  const uint64_t stride = (uint64_t)L.points_total * out_reps;
   const uint64_t gwarp = (uint64_t)blockIdx.x * kGenWarps + wib;
   const uint64_t nwarps = (uint64_t)gridDim.x * kGenWarps;
 
@@ -799,7 +800,7 @@ __global__ void __launch_bounds__(kGenThreads, Q ? 2 : BB_GEN_MINB) gen_kernel(c
       }
     }
     if (r < L.rep_end) {
-      const uint64_t o = (uint64_t)P.gidx * L.reps_total + r;
+      const uint64_t o = (uint64_t)P.gidx * out_reps + (r - L.out_rep0);
       L.out[BB_REP_THROUGHPUT * stride + o] = thr_out;
       L.out[BB_REP_LATENCY * stride + o] = lat_out;
       // without quantile mode p50/p99 are not tracked (NaN)

@@ -77,22 +77,32 @@ __global__ void thresholds_kernel(GenPoint* pts, uint32_t n_points) {
 // built without -march, i.e. without contraction).  One block per
 // point, one thread per field.
 __global__ void point_reduce_kernel(const double* __restrict__ rep, uint32_t n_points,
-                                    uint32_t reps, double* __restrict__ out) {
+                                    uint32_t reps, uint32_t chunks, double* __restrict__ out) {
   const uint32_t p = blockIdx.x, f = threadIdx.x;
   if (p >= n_points || f >= BB_REP_FIELDS) return;
-  const uint64_t stride = (uint64_t)n_points * reps;
-  const double* x = rep + f * stride + (uint64_t)p * reps;
+  // replication i lives in chunk c = the shard [R c / C, R (c+1) / C) that
+  // wrote it, laid out [field][point][its replications] at 6 P (R c / C)
+  // (chunks = 1: the plain [field][point][replication] array)
+  auto walk = [&](auto&& fn) {
+    for (uint32_t c = 0; c < chunks; ++c) {
+      const uint64_t lo = (uint64_t)reps * c / chunks, hi = (uint64_t)reps * (c + 1) / chunks;
+      const uint64_t len = hi - lo;
+      const double* x = rep + (uint64_t)BB_REP_FIELDS * n_points * lo + (uint64_t)f * n_points * len +
+                        (uint64_t)p * len;
+      for (uint64_t i = 0; i < len; ++i) fn(x[i]);
+    }
+  };
   const double nn = (double)reps;
   double sum = 0;
-  for (uint32_t i = 0; i < reps; ++i) sum = __dadd_rn(sum, x[i]);
+  walk([&](double x) { sum = __dadd_rn(sum, x); });
   const double mean = __ddiv_rn(sum, nn);
   double sd = 0;
   if (reps >= 2 && (f == BB_REP_THROUGHPUT || f == BB_REP_LATENCY)) {
     double ss = 0;
-    for (uint32_t i = 0; i < reps; ++i) {
-      const double d = __dsub_rn(x[i], mean);
+    walk([&](double x) {
+      const double d = __dsub_rn(x, mean);
       ss = __dadd_rn(ss, __dmul_rn(d, d));
-    }
+    });
     sd = __dsqrt_rn(__ddiv_rn(ss, __dsub_rn(nn, 1.0)));
   }
   double* o = out + (uint64_t)p * 8;
@@ -209,9 +219,9 @@ cudaError_t gen_run(const GenLaunch& L0, cudaStream_t s) {
 }
 
 cudaError_t gen_point_reduce(const double* rep, uint32_t n_points, uint32_t reps, double* stats,
-                             cudaStream_t s) {
+                             cudaStream_t s, uint32_t chunks) {
   if (!n_points) return cudaSuccess;
-  point_reduce_kernel<<<n_points, 32, 0, s>>>(rep, n_points, reps, stats);
+  point_reduce_kernel<<<n_points, 32, 0, s>>>(rep, n_points, reps, chunks ? chunks : 1, stats);
   note_launch();
   return cudaGetLastError();
 }

@@ -45,7 +45,9 @@ struct GenLaunch {
   int32_t svc_kind;          // SvcKind of every point in this launch
   int32_t overload;
   int32_t track;             // finite rate without flush: track open arrival sums
-  double* out;              // [BB_REP_FIELDS][n_points*reps_total]
+  double* out;              // [BB_REP_FIELDS][points_total][out_reps]
+  uint32_t out_reps;        // replications per point row of `out` (0: reps_total)
+  uint32_t out_rep0;        // replication stored in column 0 (a shard's own slice)
   AtanhCoef coef;           // exponential-variate polynomial (param space)
   uint32_t s_max;           // largest n_servers in the launch
   double* srv;              // server free times scratch (set by gen_run)
@@ -84,7 +86,10 @@ cudaError_t service_of_keys(const SvcParams& p, const uint64_t* x, uint64_t n, d
                             cudaStream_t s);
 // mean_std per point over replica order (experiment.hpp:188-200, :275-281).
 // stats_out: [n_points][8] = thr mean, thr std, lat mean, lat std, p50, p99, makespan, busy
+// chunks > 1: the array is the concatenation of `chunks` shard arrays, shard
+// c holding replications [reps c / chunks, reps (c+1) / chunks) in its own
+// [field][point][replication] layout (a gather of shard slices)
 cudaError_t gen_point_reduce(const double* rep, uint32_t n_points, uint32_t reps,
-                             double* stats_out, cudaStream_t s);
+                             double* stats_out, cudaStream_t s, uint32_t chunks = 1);
 
 }  // namespace bb

@@ -62,6 +62,10 @@ struct BBError {
 struct DevCtx {
   std::mutex mu;
   cudaStream_t stream = nullptr;
+  // stream-ordered shards (bb_*_shard_device) leave their device error flag
+  // here; the next reduce on the device reads it (one sync per sweep)
+  bb::DevError* pending = nullptr;
+  std::vector<std::pair<double, double>> pending_support;  // per point: edges front/back
 };
 DevCtx g_ctx[64];
 
@@ -969,8 +973,25 @@ void build_sweep(std::vector<bb_run_template> tpl, Sweep& W, cudaStream_t st, bo
   CK(bb::gen_setup_thresholds(W.d_pts.as<bb::GenPoint>(), (uint32_t)P, st));
 }
 
+// the message of a device-side error of sweep point `pt` (support = its edges)
+void raise_sweep_error(const bb::DevError& he, const std::pair<double, double>& support,
+                       const PointFail& pf) {
+  const size_t pt = (size_t)(he.packed >> 40);
+  char buf[256];
+  if (he.value > 0 && std::isfinite(he.value))  // binning.hpp:135-140
+    snprintf(buf, sizeof buf, "assign_bin: length %g outside bin support [%g, %g]", he.value,
+             support.first, support.second);
+  else  // simulator.hpp:189-190
+    snprintf(buf, sizeof buf, "simulation: drew a non-positive service time");
+  pf.raise_at(pt, (bb_status)(he.packed & 0xFF), buf);
+}
+
+// out_reps/out_rep0: the output rows hold replications [out_rep0, out_rep0 +
+// out_reps) (a shard's own slice; 0: the full [0, replications) rows).
+// deferred: the device error flag to use, left unchecked (stream order kept).
 void launch_sweep(const SweepParams* E, Sweep& W, uint64_t rep_begin, uint64_t rep_end,
-                  double* rep_dev, cudaStream_t st, bool time_it, const PointFail& pf = PointFail{}) {
+                  double* rep_dev, cudaStream_t st, bool time_it, const PointFail& pf = PointFail{},
+                  uint32_t out_reps = 0, uint32_t out_rep0 = 0, bb::DevError* deferred = nullptr) {
   const size_t P = W.tpl.size();
   // group points by kernel instantiation; each group's points are copied
   // (already threshold-resolved) into a contiguous device array
@@ -1033,13 +1054,20 @@ void launch_sweep(const SweepParams* E, Sweep& W, uint64_t rep_begin, uint64_t r
     L.track = keys[i].track;
     L.overload = keys[i].ovl;
     L.out = rep_dev;
+    L.out_reps = out_reps;
+    L.out_rep0 = out_rep0;
     L.quant = bb::g_gen_quantiles.load() ? 1 : 0;
     L.timers = keys[i].tm;
     L.n_max = nmax;
     L.nf_max = nfmax;
-    DBuf err(sizeof(bb::DevError), st);
-    CK(cudaMemsetAsync(err.p, 0xFF, 8, st));
-    L.err = err.as<bb::DevError>();
+    DBuf err;
+    if (deferred) {
+      L.err = deferred;
+    } else {
+      err = DBuf(sizeof(bb::DevError), st);
+      CK(cudaMemsetAsync(err.p, 0xFF, 8, st));
+      L.err = err.as<bb::DevError>();
+    }
     if (time_it && first) {
       if (!g_ev[0]) {
         CK(cudaEventCreate(&g_ev[0]));
@@ -1065,19 +1093,14 @@ void launch_sweep(const SweepParams* E, Sweep& W, uint64_t rep_begin, uint64_t r
       g_trace_ms = -1.0;
     }
     first = false;
+    if (deferred) continue;
     bb::DevError he;
     d2h(&he, err.p, sizeof he, st);
     CK(cudaStreamSynchronize(st));
     if (he.packed != ~0ull) {  // packed = (point << 40 | request << 8 | code)
       const size_t pt = (size_t)(he.packed >> 40);
       const SimSpec& s = W.spec[pt < W.spec.size() ? pt : 0];
-      char buf[256];
-      if (he.value > 0 && std::isfinite(he.value))  // binning.hpp:135-140
-        snprintf(buf, sizeof buf, "assign_bin: length %g outside bin support [%g, %g]", he.value,
-                 s.edges.front(), s.edges.back());
-      else  // simulator.hpp:189-190
-        snprintf(buf, sizeof buf, "simulation: drew a non-positive service time");
-      pf.raise_at(pt, (bb_status)(he.packed & 0xFF), buf);
+      raise_sweep_error(he, {s.edges.front(), s.edges.back()}, pf);
     }
   }
 }
@@ -1166,9 +1189,111 @@ void reference_point_reps(const SweepParams* E, const Sweep& W, std::vector<doub
   }
 }
 
+// Devices a sweep spreads over (bb_set_devices); empty: the current device.
+std::mutex g_dev_mu;
+std::vector<int> g_devices;
+
+std::vector<int> sweep_devices() {
+  std::lock_guard<std::mutex> lock(g_dev_mu);
+  return g_devices;
+}
+
+// The sweep over several devices in one process (the reference's thread pool,
+// experiment.hpp:342-368, one host thread per device): shard g of G runs
+// replications [R g / G, R (g+1) / G) of every point on devs[g] and its
+// kernels store the per-replication results straight into devs[0]'s gather
+// array (peer stores over NVLink; a device-to-device copy when peer access is
+// unavailable), in the shard's own [field][point][replication] block; devs[0]
+// then reduces every point in replication order -- the same sums as one
+// device, so the results are bit-identical for any device list.
+void run_points_multi(std::vector<bb_run_template> tpl, SweepParams E, const std::vector<int>& devs,
+                      bb_point_result* out, const PointFail& pf) {
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    raise(BB_ECUDA, "no CUDA device available (the engine has no CPU path)");
+  for (int d : devs)
+    if (d < 0 || d >= ndev) raise(BB_EINVAL, "bb_set_devices: device ordinal out of range");
+  std::vector<int> uniq(devs);
+  std::sort(uniq.begin(), uniq.end());
+  uniq.erase(std::unique(uniq.begin(), uniq.end()), uniq.end());
+  std::vector<std::unique_lock<std::mutex>> locks;
+  for (int d : uniq) locks.emplace_back(g_ctx[d].mu);  // ascending order: no lock cycles
+  const int d0 = devs[0];
+  CK(cudaSetDevice(d0));
+  cudaStream_t st0 = ctx_stream(d0);
+  const uint64_t P = tpl.size(), R = E.replications, G = devs.size();
+  if (R < G) raise(BB_EINVAL, "fewer replications than devices");
+  DBuf rep(BB_REP_FIELDS * P * R * 8, st0), stats(P * 8 * 8, st0);
+  CK(cudaStreamSynchronize(st0));  // the gather array exists before any shard writes it
+  std::vector<char> peer(ndev, 0);
+  for (int d : uniq) {
+    if (d == d0) continue;
+    int ok = 0;
+    CK(cudaDeviceCanAccessPeer(&ok, d, d0));
+    if (!ok) continue;
+    CK(cudaSetDevice(d));
+    const cudaError_t e = cudaDeviceEnablePeerAccess(d0, 0);
+    if (e == cudaSuccess || e == cudaErrorPeerAccessAlreadyEnabled) peer[d] = 1;
+    cudaGetLastError();
+  }
+  std::vector<std::exception_ptr> errs(G);
+  auto shard = [&](uint64_t g) {
+    try {
+      const int dev = devs[g];
+      CK(cudaSetDevice(dev));
+      cudaStream_t st;
+      CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+      struct StreamGuard {
+        cudaStream_t s;
+        ~StreamGuard() {
+          cudaStreamSynchronize(s);
+          cudaStreamDestroy(s);
+        }
+      } guard{st};
+      const uint64_t lo = R * g / G, hi = R * (g + 1) / G;
+      double* dst = rep.as<double>() + BB_REP_FIELDS * P * lo;  // the shard's block on d0
+      Sweep W;
+      build_sweep(tpl, W, st, true, pf);
+      if (dev == d0 || peer[dev]) {
+        launch_sweep(&E, W, lo, hi, dst, st, false, pf, (uint32_t)(hi - lo), (uint32_t)lo);
+      } else {
+        DBuf loc(BB_REP_FIELDS * P * (hi - lo) * 8, st);
+        launch_sweep(&E, W, lo, hi, loc.as<double>(), st, false, pf, (uint32_t)(hi - lo), (uint32_t)lo);
+        CK(cudaMemcpyAsync(dst, loc.p, BB_REP_FIELDS * P * (hi - lo) * 8, cudaMemcpyDefault, st));
+      }
+      CK(cudaStreamSynchronize(st));
+    } catch (...) {
+      errs[g] = std::current_exception();
+    }
+  };
+  std::vector<std::thread> pool;
+  for (uint64_t g = 1; g < G; ++g) pool.emplace_back(shard, g);
+  shard(0);
+  for (auto& t : pool) t.join();
+  for (auto& e : errs)  // the lowest shard's error, as the reference's first failure
+    if (e) std::rethrow_exception(e);
+  CK(cudaSetDevice(d0));
+  g_ev_valid = false;
+  Sweep W;
+  W.tpl = std::move(tpl);
+  for (auto& t : W.tpl) W.spec.push_back(materialize(t, 0));
+  CK(bb::gen_point_reduce(rep.as<double>(), (uint32_t)P, (uint32_t)R, stats.as<double>(), st0,
+                          (uint32_t)G));
+  std::vector<double> hs(P * 8);
+  d2h(hs.data(), stats.p, hs.size() * 8, st0);
+  CK(cudaStreamSynchronize(st0));
+  fill_points(&E, W, hs, out);
+}
+
 void run_points_host(std::vector<bb_run_template> tpl, SweepParams E, int32_t rng,
                      bb_point_result* out, const PointFail& pf = PointFail{}) {
-  const int dev = current_device(-1);
+  const std::vector<int> devs = sweep_devices();
+  if (rng != BB_RNG_REFERENCE && devs.size() > 1) {
+    if (tpl.empty()) raise(BB_EINVAL, "sweep has no points");
+    run_points_multi(std::move(tpl), E, devs, out, pf);
+    return;
+  }
+  const int dev = current_device(devs.empty() ? -1 : devs[0]);
   std::lock_guard<std::mutex> lock(g_ctx[dev].mu);
   cudaStream_t st = ctx_stream(dev);
   Sweep W;
@@ -1189,31 +1314,59 @@ void run_points_host(std::vector<bb_run_template> tpl, SweepParams E, int32_t rn
   fill_points(&E, W, hs, out);
 }
 
+// Stream-ordered shard (one process per GPU): no host synchronisation; a
+// device-side error (out-of-support service) is left in the device's pending
+// flag and raised by the next reduce on this device.
+// local: rep_dev holds only [rep_begin, rep_end) ([field][point][its reps]),
+// the block a gather of shard slices concatenates (bb_points_reduce_gathered_device).
 void points_shard(std::vector<bb_run_template> tpl, SweepParams E, uint64_t rep_begin,
-                  uint64_t rep_end, double* rep_dev, void* stream) {
+                  uint64_t rep_end, double* rep_dev, void* stream, bool local = false) {
   if (rep_end > E.replications || rep_begin > rep_end) raise(BB_EINVAL, "bad replication range");
   const int dev = current_device(-1);
   std::lock_guard<std::mutex> lock(g_ctx[dev].mu);
   cudaStream_t st = stream ? (cudaStream_t)stream : ctx_stream(dev);
+  DevCtx& C = g_ctx[dev];
+  if (!C.pending) {
+    CK(cudaMalloc((void**)&C.pending, sizeof(bb::DevError)));
+    CK(cudaMemsetAsync(C.pending, 0xFF, 8, st));
+  }
   Sweep W;
   build_sweep(std::move(tpl), W, st);
-  if (rep_end > rep_begin) launch_sweep(&E, W, rep_begin, rep_end, rep_dev, st, true);
+  C.pending_support.clear();
+  for (const SimSpec& sp : W.spec) C.pending_support.push_back({sp.edges.front(), sp.edges.back()});
+  if (rep_end > rep_begin)
+    launch_sweep(&E, W, rep_begin, rep_end, rep_dev, st, true, PointFail{},
+                 local ? (uint32_t)(rep_end - rep_begin) : 0u, local ? (uint32_t)rep_begin : 0u,
+                 C.pending);
 }
 
+// chunks > 1: rep_dev is a gather of `chunks` shard slices (see gen_point_reduce)
 void points_reduce(std::vector<bb_run_template> tpl, SweepParams E, const double* rep_dev,
-                   bb_point_result* out, void* stream) {
+                   bb_point_result* out, void* stream, uint32_t chunks = 1) {
   const int dev = current_device(-1);
   std::lock_guard<std::mutex> lock(g_ctx[dev].mu);
   cudaStream_t st = stream ? (cudaStream_t)stream : ctx_stream(dev);
+  DevCtx& C = g_ctx[dev];
   Sweep W;
   W.tpl = std::move(tpl);
   for (auto& t : W.tpl) W.spec.push_back(materialize(t, 0));
   const uint64_t P = W.tpl.size();
   DBuf stats(P * 8 * 8, st);
-  CK(bb::gen_point_reduce(rep_dev, (uint32_t)P, (uint32_t)E.replications, stats.as<double>(), st));
+  CK(bb::gen_point_reduce(rep_dev, (uint32_t)P, (uint32_t)E.replications, stats.as<double>(), st,
+                          chunks));
   std::vector<double> hs(P * 8);
   d2h(hs.data(), stats.p, hs.size() * 8, st);
+  bb::DevError he{~0ull, 0.0, 0};
+  if (C.pending) d2h(&he, C.pending, sizeof he, st);
   CK(cudaStreamSynchronize(st));
+  if (he.packed != ~0ull) {  // a shard on this device failed: report it here
+    CK(cudaMemsetAsync(C.pending, 0xFF, 8, st));
+    CK(cudaStreamSynchronize(st));
+    const size_t pt = (size_t)(he.packed >> 40);
+    raise_sweep_error(he, pt < C.pending_support.size() ? C.pending_support[pt]
+                                                         : std::pair<double, double>{0.0, 0.0},
+                      PointFail{});
+  }
   fill_points(&E, W, hs, out);
 }
 
@@ -1368,6 +1521,41 @@ bb_status bb_points_shard_device(const bb_run_template* points, uint64_t n_point
     if (!points || !n_points) raise(BB_EINVAL, "empty point list");
     points_shard(std::vector<bb_run_template>(points, points + n_points),
                  SweepParams{seed, replications}, rep_begin, rep_end, rep_metrics_dev, stream);
+  });
+}
+
+bb_status bb_points_shard_local_device(const bb_run_template* points, uint64_t n_points,
+                                       uint64_t replications, uint64_t seed, uint64_t rep_begin,
+                                       uint64_t rep_end, double* shard_dev, void* stream) {
+  return guarded([&] {
+    if (!points || !n_points) raise(BB_EINVAL, "empty point list");
+    points_shard(std::vector<bb_run_template>(points, points + n_points),
+                 SweepParams{seed, replications}, rep_begin, rep_end, shard_dev, stream, true);
+  });
+}
+
+bb_status bb_points_reduce_gathered_device(const bb_run_template* points, uint64_t n_points,
+                                           uint64_t replications, uint32_t n_shards,
+                                           const double* gathered_dev, bb_point_result* out,
+                                           void* stream) {
+  return guarded([&] {
+    if (!points || !n_points) raise(BB_EINVAL, "empty point list");
+    if (n_shards < 1 || n_shards > replications) raise(BB_EINVAL, "bad shard count");
+    points_reduce(std::vector<bb_run_template>(points, points + n_points),
+                  SweepParams{0, replications}, gathered_dev, out, stream, n_shards);
+  });
+}
+
+bb_status bb_set_devices(const int32_t* devices, uint32_t n) {
+  return guarded([&] {
+    if (n && !devices) raise(BB_EINVAL, "bb_set_devices: null device list");
+    int ndev = 0;
+    if (n && (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0))
+      raise(BB_ECUDA, "no CUDA device available (the engine has no CPU path)");
+    for (uint32_t i = 0; i < n; ++i)
+      if (devices[i] < 0 || devices[i] >= ndev) raise(BB_EINVAL, "bb_set_devices: device ordinal out of range");
+    std::lock_guard<std::mutex> lock(g_dev_mu);
+    g_devices.assign(devices, devices + n);
   });
 }
 

@@ -195,9 +195,76 @@ struct QFast {
   const double* F;      // its completions by batch id
   uint32_t n, lane;
 
-  // indices of the requests whose bucket is one of want[0..3] (0xFFFFFFFF:
-  // unused) into slots[] as raw 64-bit words; returns how many
-  __device__ uint32_t collect(const uint32_t want[4], unsigned long long* slots) const {
+  // Level 0 of the selection in one lean pass over the log: every request's
+  // latency F[id] - a (the reference's subtraction), their sum, a histogram
+  // of b = min((hi32(key) - hbase) >> s, 2047) -- a monotone function of the
+  // key, so every bucket is a contiguous key range [(hbase + b 2^s) 2^32,
+  // + 2^(s+32)) -- and b itself per request (0xFFFF: never completed) for
+  // the collect pass.  A lane reads request t*32 + lane of the replication,
+  // so each run of 32 is one 256 B (arrivals) + 128 B (ids) access; 32-bit
+  // offsets, no predication outside the ragged last run.
+  __device__ double level0(uint32_t* hist, uint32_t hbase, uint32_t s) const {
+    const uint32_t full = n / 32, nt = (n + 31) / 32;
+    const double* a_p = A + lane;
+    const uint32_t* i_p = Id + lane;
+    uint16_t* k_p = Bk + lane;
+    double acc = 0.0;
+    auto one = [&](double a, double f, bool valid, uint32_t off) {
+      const double x = __dsub_rn(f, a);
+      const bool done = valid && x == x;  // NaN: the batch never completed
+      uint32_t b = 0xFFFFu;
+      if (done) {
+        b = min((uint32_t)(__double2hiint(x) - (int)hbase) >> s, kQBuckets - 1);
+        atomicAdd(&hist[b], 1u);
+        acc += x;
+      }
+      if (valid) k_p[off] = (uint16_t)b;
+    };
+    // software pipeline: the next chunk's arrivals and ids are in flight
+    // while this chunk's completions are gathered and used
+    constexpr int C = kQChunk;
+    uint32_t t = 0;
+    double na[C];
+    uint32_t nid[C];
+    if (C <= full) {
+#pragma unroll
+      for (int u = 0; u < C; ++u) {
+        na[u] = a_p[u * (32 * kQRun)];
+        nid[u] = i_p[u * (32 * kQRun)];
+      }
+    }
+    for (; t + C <= full; t += C) {
+      double a[C], f[C];
+#pragma unroll
+      for (int u = 0; u < C; ++u) {
+        a[u] = na[u];
+        f[u] = F[nid[u]];
+      }
+      if (t + 2 * C <= full) {
+#pragma unroll
+        for (int u = 0; u < C; ++u) {
+          na[u] = a_p[(t + C + u) * (32 * kQRun)];
+          nid[u] = i_p[(t + C + u) * (32 * kQRun)];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < C; ++u) one(a[u], f[u], true, (t + u) * (32 * kQRun));
+    }
+    for (; t < nt; ++t) {
+      const bool v = t * 32 + lane < n;
+      one(v ? a_p[t * (32 * kQRun)] : 0.0, v ? F[i_p[t * (32 * kQRun)]] : 0.0, v, t * (32 * kQRun));
+    }
+    return acc;
+  }
+
+  // indices of the requests whose level-0 bucket lies in [w0, w0 + d0] or
+  // [w2, w2 + d2] into slots[] (raw 64-bit words); returns how many.  The
+  // ranges are exact (the buckets of ranks i and i+1 are equal or every
+  // bucket between them is empty), and hits are sparse: a lane tests its
+  // eight buckets with two range compares each and the warp only places
+  // hits when some lane has one.
+  __device__ uint32_t collect(uint32_t w0, uint32_t d0, uint32_t w2, uint32_t d2,
+                              unsigned long long* slots) const {
     static_assert(kQRun % 8 == 0, "eight buckets per lane load");
     constexpr int G = 4;  // loads in flight per lane
     const uint32_t ng = (n + 7) / 8;  // groups of 8 requests
@@ -213,17 +280,29 @@ struct QFast {
 #pragma unroll
       for (int u = 0; u < G; ++u) {
         const uint32_t w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+        const uint32_t base = (g0 + u * 32 + lane) * 8;
+        uint32_t hm = 0;
 #pragma unroll
         for (int h = 0; h < 8; ++h) {
           const uint32_t bk = (w[h >> 1] >> (16 * (h & 1))) & 0xFFFFu;
-          const bool hit = (bk == want[0] || bk == want[1] || bk == want[2] || bk == want[3]) &&
-                           (g0 + u * 32 + lane) * 8 + h < n;  // (padding is never written)
-          const uint32_t hm = __ballot_sync(kQFull, hit);
-          if (hit)
-            slots[nc + __popc(hm & ((1u << lane) - 1u))] =
-                (unsigned long long)((g0 + u * 32 + lane) * 8 + h);
-          nc += __popc(hm);
+          hm |= (uint32_t)((bk - w0 <= d0) | (bk - w2 <= d2)) << h;
         }
+        if (base + 8 > n) hm &= base < n ? (1u << (n - base)) - 1u : 0u;  // (padding is never written)
+        if (!__any_sync(kQFull, hm != 0)) continue;
+        const uint32_t c = __popc(hm);
+        uint32_t pre = c;  // inclusive scan of the hit counts over the lanes
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(kQFull, pre, o);
+          if (lane >= (uint32_t)o) pre += y;
+        }
+        uint32_t at = nc + pre - c;
+        while (hm) {
+          const uint32_t h = __ffs(hm) - 1;
+          hm &= hm - 1;
+          slots[at++] = (unsigned long long)(base + h);
+        }
+        nc += __shfl_sync(kQFull, pre, 31);
       }
     }
     return nc;
@@ -279,7 +358,6 @@ __device__ void q_select(Src1& first, const Src& src, uint64_t m, double lmin, d
     for (uint32_t j = lane; j < kQBuckets; j += 32) hist[j] = 0;
     __syncwarp();
     const uint64_t gw = qwidth(gsh);
-    const bool keep = qf && gsh >= 64;  // level 0: remember every request's bucket
     double acc = 0.0;
     source.for_each([&](double x, uint32_t w, uint32_t i) {
       if (sum && w) acc += x * (double)w;
@@ -290,7 +368,6 @@ __device__ void q_select(Src1& first, const Src& src, uint64_t m, double lmin, d
         b16 = (uint32_t)(bk < kQBuckets ? bk : kQBuckets - 1);
         atomicAdd(&hist[b16], w);
       }
-      if (keep && i < qf->n) qf->Bk[qlog_index(i)] = (uint16_t)b16;
     });
     if (sum) {
 #pragma unroll
@@ -336,29 +413,71 @@ __device__ void q_select(Src1& first, const Src& src, uint64_t m, double lmin, d
     __syncwarp();
   };
 
-  refine(first, kbase, 64, wsum != nullptr);
+  uint32_t hb = 0, hs = 0;  // request log: level-0 buckets over the keys' high words
+  if (qf) {
+    hb = (uint32_t)(kbase >> 32);
+    const uint32_t hspan = (uint32_t)(qkey(lmax) >> 32) - hb;
+    while ((hspan >> hs) >= kQBuckets) ++hs;
+    for (uint32_t j = lane; j < kQBuckets; j += 32) hist[j] = 0;
+    __syncwarp();
+    double acc = qf->level0(hist, hb, hs);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(kQFull, acc, o);
+    if (wsum) *wsum = acc;
+    __syncwarp();
+    // bucket b holds the keys [(hb + b 2^hs) 2^32, + 2^(hs+32))
+    uint32_t loc = 0;
+    for (uint32_t j = 0; j < kQBuckets / 32; ++j) loc += hist[lane * (kQBuckets / 32) + j];
+    uint32_t pre = loc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t v = __shfl_up_sync(kQFull, pre, o);
+      if (lane >= (uint32_t)o) pre += v;
+    }
+    pre -= loc;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const uint64_t r = rk[t];
+      const bool mine = r >= pre && r < (uint64_t)pre + loc;
+      const uint32_t who = __ffs(__ballot_sync(kQFull, mine)) - 1;
+      uint32_t b = 0, c = 0, h = 0;
+      if (mine) {
+        c = pre;
+        for (uint32_t j = 0; j < kQBuckets / 32; ++j) {
+          h = hist[lane * (kQBuckets / 32) + j];
+          if (r < (uint64_t)c + h) {
+            b = lane * (kQBuckets / 32) + j;
+            break;
+          }
+          c += h;
+        }
+      }
+      b = __shfl_sync(kQFull, b, who);
+      klo[t] = (uint64_t)(hb + (b << hs)) << 32;
+      sh[t] = hs + 32;
+      below[t] = __shfl_sync(kQFull, c, who);
+      cnt[t] = __shfl_sync(kQFull, h, who);
+    }
+    __syncwarp();
+  } else {
+    refine(first, kbase, 64, wsum != nullptr);
+  }
   // fast path: the level-0 buckets of the wanted ranks hold few enough values
   bool fast = false;
   if (qf) {
-    uint64_t total = 0;
-    uint32_t want[4] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu};
-    bool ok = true;
-#pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      ok &= sh[t] == sh0 && sh0 > 0;
-      bool dup = false;
-#pragma unroll
-      for (int u = 0; u < t; ++u) dup |= klo[u] == klo[t];
-      if (!dup) {
-        total += cnt[t];
-        want[t] = (uint32_t)((klo[t] - kbase) >> sh0);
-      }
-    }
-    if (ok && total <= cap) {
+    uint64_t total = cnt[0] + cnt[2];
+    if (klo[1] != klo[0]) total += cnt[1];
+    if (klo[3] != klo[2]) total += cnt[3];
+    if (klo[2] == klo[0] || klo[2] == klo[1]) total -= cnt[2];
+    if (klo[3] != klo[2] && (klo[3] == klo[0] || klo[3] == klo[1])) total -= cnt[3];
+    if (total <= cap) {
       fast = true;
       __syncwarp();  // the histogram is done with; the region holds candidates
       unsigned long long* slots = reinterpret_cast<unsigned long long*>(cx);
-      const uint32_t ncol = qf->collect(want, slots);
+      // buckets of ranks i and i+1: equal, or every bucket between them empty
+      const uint32_t b0 = (uint32_t)((klo[0] >> 32) - hb) >> hs, b1 = (uint32_t)((klo[1] >> 32) - hb) >> hs;
+      const uint32_t b2 = (uint32_t)((klo[2] >> 32) - hb) >> hs, b3 = (uint32_t)((klo[3] >> 32) - hb) >> hs;
+      const uint32_t ncol = qf->collect(b0, b1 - b0, b2, b3 - b2, slots);
       __syncwarp();
       for (uint32_t c = lane; c < ncol; c += 32) {
         const double x = qf->latency((uint32_t)slots[c]);
