@@ -28,39 +28,17 @@
 namespace bb {
 namespace {
 
-#ifndef BB_PART_MATCH
-#define BB_PART_MATCH 1  // stable in-warp ranks by match_any (0: one ballot per bin)
-#endif
-#ifndef BB_PART_IPT
-#define BB_PART_IPT 8
-#endif
-constexpr int TB = 256, IPT = BB_PART_IPT, TILE = TB * IPT, NW = TB / 32;
-constexpr unsigned long long FLAG_A = 1ull << 62, FLAG_P = 2ull << 62, VAL_MASK = (1ull << 62) - 1;
 constexpr unsigned long long KEY_UNSERVED = ~0ull;
 constexpr uint32_t FL_NONMONO = 1, FL_TIE_GT_B = 2, FL_NOT_ALL_EQUAL = 4;
 constexpr int LB = 256, LI = 8, LTILE = LB * LI;  // Lindley scan tile
 constexpr int HBITS = 12, HBINS = 1 << HBITS;
-constexpr int kLookWin = 8;  // predecessors per look-back round trip (packed words: relaxed loads)
 
-__device__ __forceinline__ void st_release64(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long ld_acquire64(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
 __device__ __forceinline__ void st_release32(uint32_t* p, uint32_t v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 __device__ __forceinline__ uint32_t ld_acquire32(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ unsigned long long ld_relaxed64(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
 __device__ __forceinline__ uint32_t lanemask_lt() {
@@ -81,20 +59,19 @@ struct Info {
   uint32_t cfirst[BB_TRACE_MAX_BINS];     // overload: closing index of batch (b,0)
   uint32_t tpos[BB_TRACE_MAX_BINS];       // overload + timers: timer batch position after the closings
   uint32_t treq[BB_TRACE_MAX_BINS];       //   ... and requests in timer batches before it
+  uint32_t sbase[BB_TRACE_MAX_BINS];      // first batch-maximum slot (WS::smax) of bin b
 };
 
 struct WS {
-  uint32_t* counters;            // [0] partition tiles, [1] lindley tiles
-  unsigned long long* desc1;     // [ntiles*k] flag(2 bits) | count
-  unsigned long long* desc2v;    // [ntiles*k] alpha<<63 | open-max bits
-  uint32_t* desc2f;              // [ntiles*k]
+  uint32_t* counters;            // [1] lindley tiles, [2] binade tiles
+  uint32_t* tcount;              // [k][ntiles] per-tile bin counts -> exclusive tile prefixes
+  unsigned long long* smax;      // batch services (IEEE bits) at sbase[bin] + j
   uint8_t* pb8;
   uint32_t* rank;
-  double *recR, *recS;
+  double* recR;
   uint8_t* recBin;
   uint32_t *recJ, *recC;
-  unsigned long long* fin_cnt;   // [k]
-  unsigned long long* fin_open;  // [k] double bits
+  unsigned long long* fin_cnt;   // [k] requests per bin
   uint32_t* flags;
   DevError* err;
   Info* info;
@@ -128,337 +105,321 @@ __device__ __forceinline__ uint32_t assign_bin(const double* e, uint32_t k, doub
   return lo;
 }
 
-__global__ void __launch_bounds__(TB) partition_kernel(PartArgs P) {
+// ----------------------------------------------------------- K2 partition
+// Three streaming passes over the requests -- no look-back chain, so no tile
+// waits for another:
+//   count_kernel  per tile of PTILE requests: the predicted bin of every
+//                 request (written to pb8 when it is drawn from u_err; a given
+//                 pred[] is used in place), per-bin counts by warp ballots
+//   tscan_kernel  per bin: exclusive prefix of the tile counts (in place),
+//                 totals, and the slot base of each bin's batch maxima
+//   place_kernel  per tile: service checks, stable rank of every request in
+//                 its bin (tile prefix + in-warp match_any ranks), batch
+//                 service = max over the members (fragment maxima in shared
+//                 memory, then one global atomicMax per (bin, batch) fragment
+//                 on the IEEE bits of the positive services), closing records
+//                 in closing-request order (closings before the tile are
+//                 sum_b floor(prefix_b / B))
+constexpr int PT = 256, PIPT = 8, PTILE = PT * PIPT, PNW = PT / 32;
+
+// the predicted bin of request idx (0: invalid, error raised); tb: true bin
+__device__ __forceinline__ uint32_t part_bin(const PartArgs& P, const double* edges, uint64_t idx,
+                                             double sv, uint32_t& tb) {
+  const uint32_t k = P.k;
+  tb = 0;
+  if (!(sv > 0) || !isfinite(sv)) {
+    raise_error(P.ws.err, idx, BB_EDOMAIN, sv, 1);  // simulator.hpp:189-190
+    return 0;
+  }
+  if ((tb = assign_bin(edges, k, sv)) == 0) {
+    raise_error(P.ws.err, idx, BB_EDOMAIN, sv, 2);  // binning.hpp:135-140
+    return 0;
+  }
+  if (P.err_kind == 1) {  // Symmetric, binning.hpp:238-246
+    const double u = P.u_err[idx];
+    if (tb == 1) return u < P.p ? 2 : 1;
+    if (tb == k) return u < P.p ? k - 1 : k;
+    if (u < P.p) return tb - 1;
+    if (u >= P.one_minus_p) return tb + 1;
+    return tb;
+  }
+  if (P.err_kind == 2) {  // Confusion, binning.hpp:247-257
+    const double u = P.u_err[idx];
+    const double* row = P.conf + (uint64_t)(tb - 1) * k;
+    double cum = 0.0;
+    for (uint32_t q = 0; q < k; ++q) {
+      cum = __dadd_rn(cum, row[q]);
+      if (u < cum) return q + 1;
+    }
+    return k;
+  }
+  return tb;
+}
+
+__global__ void __launch_bounds__(PT) count_kernel(PartArgs P) {
   __shared__ double s_edges[BB_TRACE_MAX_BINS + 1];
-  __shared__ uint32_t s_wcnt[NW][32], s_woff[NW][32];
-  __shared__ uint32_t s_excl[32], s_tot[32], s_jlo[32], s_fbase[32], s_nfrag[32];
-  __shared__ unsigned long long s_slot[TILE + 32];
-  __shared__ uint32_t s_wclose[NW];
-  __shared__ uint32_t s_closebase, s_tile, s_flags, s_nfrag_total;
-  __shared__ unsigned long long s_lbsum[NW][32], s_acc[32];
-  __shared__ uint8_t s_lbfound[NW][32], s_bdone[32];
-  __shared__ int s_lbdone;
+  __shared__ uint32_t s_cnt[PNW][32];
+  const uint32_t tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const uint32_t k = P.k, n = P.n;
+  for (uint32_t i = tid; i <= k; i += PT) s_edges[i] = P.edges[i];
+  s_cnt[w][lane] = 0;
+  __syncthreads();
+  const uint64_t base = (uint64_t)blockIdx.x * PTILE + w * (32 * PIPT);
+#pragma unroll 4
+  for (int j = 0; j < PIPT; ++j) {
+    const uint64_t idx = base + j * 32 + lane;
+    uint32_t b = 0;
+    if (idx < n) {
+      if (P.pred) {
+        b = P.pred[idx];
+        if (b < 1 || b > k) {
+          raise_error(P.ws.err, idx, BB_EINVAL, (double)b, 3);
+          b = 0;
+        }
+      } else {
+        uint32_t tb;
+        b = part_bin(P, s_edges, idx, P.s[idx], tb);
+        P.ws.pb8[idx] = (uint8_t)b;
+        if (P.tb_out) P.tb_out[idx] = (uint8_t)tb;
+      }
+    }
+    const uint32_t peers = __match_any_sync(0xffffffffu, b);  // the bin's lowest lane adds them
+    if (b && !(peers & lanemask_lt())) s_cnt[w][b - 1] += __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  if (w == 0 && lane < k) {
+    uint32_t c = 0;
+    for (int w2 = 0; w2 < PNW; ++w2) c += s_cnt[w2][lane];
+    P.ws.tcount[(uint64_t)lane * P.ntiles + blockIdx.x] = c;  // bin-major: a bin's tiles contiguous
+  }
+}
+
+// one block per bin: exclusive scan of its row of tile counts (each thread a
+// contiguous run of tiles, all loads in flight, one block-wide scan)
+constexpr int TS_T = 1024, TS_R = 8;  // threads, tiles per thread per round
+__global__ void __launch_bounds__(TS_T) tscan_kernel(WS ws, uint32_t ntiles, uint32_t k, uint32_t B) {
+  __shared__ uint32_t s_w[TS_T / 32];
+  __shared__ uint32_t s_carry;
+  const uint32_t tid = threadIdx.x, lane = tid & 31, w = tid >> 5, b = blockIdx.x;
+  uint32_t* row = ws.tcount + (uint64_t)b * ntiles;
+  if (tid == 0) s_carry = 0;
+  for (uint32_t t0 = 0; t0 < ntiles; t0 += TS_T * TS_R) {
+    uint32_t v[TS_R], sum = 0;
+#pragma unroll
+    for (int r = 0; r < TS_R; ++r) {
+      const uint32_t t = t0 + tid * TS_R + r;
+      v[r] = t < ntiles ? row[t] : 0u;
+      sum += v[r];
+    }
+    uint32_t x = sum;  // inclusive scan of the thread sums
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= (uint32_t)o) x += y;
+    }
+    __syncthreads();  // s_carry of the previous round is final
+    if (lane == 31) s_w[w] = x;
+    __syncthreads();
+    if (w == 0) {
+      uint32_t y = s_w[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t z = __shfl_up_sync(0xffffffffu, y, o);
+        if (lane >= (uint32_t)o) y += z;
+      }
+      s_w[lane] = y - s_w[lane];  // exclusive warp offsets
+    }
+    __syncthreads();
+    uint32_t run = s_carry + s_w[w] + x - sum;
+#pragma unroll
+    for (int r = 0; r < TS_R; ++r) {
+      const uint32_t t = t0 + tid * TS_R + r;
+      if (t < ntiles) row[t] = run;
+      run += v[r];
+    }
+    __syncthreads();
+    if (tid == TS_T - 1) s_carry = run;
+  }
+  __syncthreads();
+  if (tid == 0) ws.fin_cnt[b] = s_carry;
+}
+
+// batch-maximum slots: floor(total / B) full + 1 open batch per bin
+__global__ void sbase_kernel(WS ws, uint32_t k, uint32_t B) {
+  uint32_t acc = 0;
+  for (uint32_t q = 0; q < k; ++q) {
+    ws.info->sbase[q] = acc;
+    acc += (uint32_t)ws.fin_cnt[q] / B + 1;
+  }
+}
+
+template <bool TBOUT>  // true bins requested with given predictions (detail output)
+__global__ void __launch_bounds__(PT, 3) place_kernel(PartArgs P) {
+  __shared__ double s_edges[BB_TRACE_MAX_BINS + 1];
+  __shared__ uint32_t s_run[PNW][32], s_woff[PNW][32];
+  __shared__ uint32_t s_excl[32], s_sbase[32], s_jlo[32], s_fbase[32];
+  __shared__ uint32_t s_shi[PTILE + 32], s_slo[PTILE + 32];  // fragment maxima: high, low words
+  __shared__ uint32_t s_wclose[PNW];
+  __shared__ uint32_t s_closebase, s_flags, s_nfrag_total;
 
   const uint32_t tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const uint32_t k = P.k, n = P.n, B = P.B;
-  if (tid == 0) {
-    s_tile = atomicAdd(&P.ws.counters[0], 1u);
-    s_flags = 0;
+  const uint32_t k = P.k, n = P.n, B = P.B, t = blockIdx.x;
+  const Info* I = P.ws.info;
+  for (uint32_t i = tid; i <= k; i += PT) s_edges[i] = P.edges[i];
+  if (w == 0) {
+    uint32_t jlo = 0, nfrag = 0;
+    if (lane < k) {
+      const uint32_t excl = P.ws.tcount[(uint64_t)lane * P.ntiles + t];
+      const uint32_t nxt = t + 1 < P.ntiles ? P.ws.tcount[(uint64_t)lane * P.ntiles + t + 1]
+                                            : (uint32_t)P.ws.fin_cnt[lane];
+      jlo = P.divB.div(excl);
+      nfrag = nxt > excl ? P.divB.div(nxt - 1) - jlo + 1 : 0;  // batches this tile touches
+      s_excl[lane] = excl;
+      s_jlo[lane] = jlo;
+      s_sbase[lane] = I->sbase[lane];
+    }
+    uint32_t incl = nfrag;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= (uint32_t)o) incl += v;
+    }
+    if (lane < k) s_fbase[lane] = incl - nfrag;
+    if (lane == 31) s_nfrag_total = incl;
+    uint32_t cb = lane < k ? jlo : 0;  // closings before this tile = sum_b floor(excl_b / B)
+#pragma unroll
+    for (int o = 16; o; o >>= 1) cb += __shfl_xor_sync(0xffffffffu, cb, o);
+    if (lane == 0) {
+      s_closebase = cb;
+      s_flags = 0;
+    }
   }
-  for (uint32_t i = tid; i <= k; i += TB) s_edges[i] = P.edges[i];
+  s_run[w][lane] = 0;
   __syncthreads();
-  const uint32_t t = s_tile;
-  const uint64_t wbase = (uint64_t)t * TILE + w * (32 * IPT);
+  for (uint32_t i = tid; i < s_nfrag_total; i += PT) s_shi[i] = s_slo[i] = 0u;
 
-  double av[IPT], sv[IPT];
-  uint32_t pb[IPT], rl[IPT];
-#pragma unroll
-  for (int j = 0; j < IPT; ++j) {
-    const uint64_t idx = wbase + j * 32 + lane;
-    av[j] = idx < n ? P.a[idx] : 0.0;
-    sv[j] = idx < n ? P.s[idx] : 0.0;
-  }
+  const uint64_t wbase = (uint64_t)t * PTILE + w * (32 * PIPT);
   const double a0 = P.a[0];
-  uint32_t flags = 0;
+  const uint8_t* pbsrc = P.pred ? P.pred : P.ws.pb8;
+  double av[PIPT], sv[PIPT];
+  uint32_t pr[PIPT];  // predicted bin | rank within the warp's requests of that bin << 8
 #pragma unroll
-  for (int j = 0; j < IPT; ++j) {
+  for (int j = 0; j < PIPT; ++j) {
+    const uint64_t idx = wbase + j * 32 + lane;
+    const bool v = idx < n;
+    av[j] = v ? P.a[idx] : 0.0;
+    sv[j] = v ? P.s[idx] : 0.0;
+    pr[j] = v ? pbsrc[idx] : 0u;
+  }
+  uint32_t flags = 0;
+  const uint32_t lt = lanemask_lt();
+#pragma unroll
+  for (int j = 0; j < PIPT; ++j) {
     const uint64_t idx = wbase + j * 32 + lane;
     const bool valid = idx < n;
+    const uint32_t pb = pr[j];
     // predecessor arrival for the monotonicity / tie checks
     double prev = __shfl_up_sync(0xffffffffu, av[j], 1);
     const double prevj = __shfl_sync(0xffffffffu, av[j > 0 ? j - 1 : 0], 31);
     if (lane == 0) prev = j > 0 ? prevj : (idx > 0 && valid ? P.a[idx - 1] : av[j]);
-    uint32_t tb = 0, b = 0;
     if (valid) {
       if (idx > 0) {
         if (!(av[j] >= prev)) flags |= FL_NONMONO;
         else if (av[j] == prev && idx >= B && P.a[idx - B] == av[j]) flags |= FL_TIE_GT_B;
       }
       if (av[j] != a0) flags |= FL_NOT_ALL_EQUAL;
-      const double s = sv[j];
-      if (!(s > 0) || !isfinite(s)) {
-        raise_error(P.ws.err, idx, BB_EDOMAIN, s, 1);  // simulator.hpp:189-190
-      } else if ((tb = assign_bin(s_edges, k, s)) == 0) {
-        raise_error(P.ws.err, idx, BB_EDOMAIN, s, 2);  // binning.hpp:135-140
-      } else if (P.pred) {
-        b = P.pred[idx];
-        if (b < 1 || b > k) {
-          raise_error(P.ws.err, idx, BB_EINVAL, (double)b, 3);
-          b = 0;
-        }
-      } else if (P.err_kind == 1) {  // Symmetric, binning.hpp:238-246
-        const double u = P.u_err[idx];
-        if (tb == 1) b = u < P.p ? 2 : 1;
-        else if (tb == k) b = u < P.p ? k - 1 : k;
-        else if (u < P.p) b = tb - 1;
-        else if (u >= P.one_minus_p) b = tb + 1;
-        else b = tb;
-      } else if (P.err_kind == 2) {  // Confusion, binning.hpp:247-257
-        const double u = P.u_err[idx];
-        const double* row = P.conf + (uint64_t)(tb - 1) * k;
-        double cum = 0.0;
-        b = k;
-        for (uint32_t q = 0; q < k; ++q) {
-          cum = __dadd_rn(cum, row[q]);
-          if (u < cum) {
-            b = q + 1;
-            break;
-          }
-        }
-      } else {
-        b = tb;
+      if (P.pred) {  // given predictions: the services are still checked (and binned)
+        uint32_t tb = 0;
+        const double s = sv[j];
+        if (!(s > 0) || !isfinite(s)) raise_error(P.ws.err, idx, BB_EDOMAIN, s, 1);
+        else if (TBOUT ? (tb = assign_bin(s_edges, k, s)) == 0 : !(s >= s_edges[0] && s <= s_edges[k]))
+          raise_error(P.ws.err, idx, BB_EDOMAIN, s, 2);
+        if (TBOUT) P.tb_out[idx] = (uint8_t)tb;
       }
-      if (P.tb_out) P.tb_out[idx] = (uint8_t)tb;
     }
-    pb[j] = b;
+    // stable rank within the warp's requests of the same bin (match_any)
+    const uint32_t peers = __match_any_sync(0xffffffffu, pb);
+    const uint32_t mine = pb ? peers : 0u;
+    const uint32_t run = pb ? s_run[w][pb - 1] : 0u;
+    pr[j] = pb | ((run + __popc(mine & lt)) << 8);
+    __syncwarp();
+    if (pb && !(mine & lt)) s_run[w][pb - 1] = run + __popc(mine);
+    __syncwarp();
   }
   if (flags) atomicOr(&s_flags, flags);
-
-  // stable rank within the warp's 256 consecutive requests: one ballot per bin
-  uint32_t wc = 0;  // lane b: running count of bin b+1 in this warp
-#if BB_PART_MATCH
-  // peers by __match_any_sync; each bin's lowest lane publishes the bin's count
-  const uint32_t lt = lanemask_lt();
-#pragma unroll
-  for (int j = 0; j < IPT; ++j) {
-    const uint32_t peers = __match_any_sync(0xffffffffu, pb[j]);
-    const uint32_t mine = pb[j] ? peers : 0u;
-    if (lane < k) s_wcnt[w][lane] = 0;
-    __syncwarp();
-    if (pb[j] && !(mine & lt)) s_wcnt[w][pb[j] - 1] = __popc(mine);
-    __syncwarp();
-    const uint32_t own = lane < k ? s_wcnt[w][lane] : 0u;
-    __syncwarp();
-    const uint32_t basec = __shfl_sync(0xffffffffu, wc, pb[j] ? pb[j] - 1 : 0);
-    rl[j] = basec + __popc(mine & lt);
-    wc += own;
-  }
-#else
-#pragma unroll
-  for (int j = 0; j < IPT; ++j) {
-    uint32_t mine = 0, own = 0;
-    for (uint32_t b = 1; b <= k; ++b) {
-      const uint32_t bal = __ballot_sync(0xffffffffu, pb[j] == b);
-      if (pb[j] == b) mine = bal;
-      if (lane == b - 1) own = bal;
-    }
-    const uint32_t basec = __shfl_sync(0xffffffffu, wc, pb[j] ? pb[j] - 1 : 0);
-    rl[j] = basec + __popc(mine & lanemask_lt());
-    wc += __popc(own);
-  }
-#endif
-  if (lane < k) s_wcnt[w][lane] = wc;
   __syncthreads();
+  if (w == 0 && lane < k) {  // warp offsets within the tile
+    uint32_t acc = 0;
+    for (int w2 = 0; w2 < PNW; ++w2) {
+      s_woff[w2][lane] = acc;
+      acc += s_run[w2][lane];
+    }
+  }
   if (tid == 0 && s_flags) atomicOr(P.ws.flags, s_flags);
-
-  if (w == 0 && lane < k) {
-    uint32_t run = 0;
-    for (int w2 = 0; w2 < NW; ++w2) {
-      s_woff[w2][lane] = run;
-      run += s_wcnt[w2][lane];
-    }
-    s_tot[lane] = run;
-    st_release64(P.ws.desc1 + (uint64_t)t * k + lane, (t == 0 ? FLAG_P : FLAG_A) | run);
-  }
-  if (tid < 32) {
-    s_acc[tid] = 0;
-    s_bdone[tid] = tid >= k;
-  }
-  __syncthreads();
-  // phase-1 decoupled look-back with the whole block: warp w inspects
-  // predecessors base-w*kLookWin .. base-w*kLookWin-(kLookWin-1), one bin
-  // per lane, so a round trip covers NW*kLookWin predecessors; the windows
-  // are combined nearest-first in shared memory and stop at the first
-  // inclusive prefix of each bin.
-  if (t > 0) {
-    int64_t base = (int64_t)t - 1;
-    while (true) {
-      unsigned long long sum = 0;
-      uint8_t found = 0;
-      if (lane < k && !s_bdone[lane]) {
-        const int64_t p0 = base - (int64_t)w * kLookWin;
-        unsigned long long v[kLookWin];
-#pragma unroll
-        for (int i = 0; i < kLookWin; ++i)
-          v[i] = p0 - i >= 0 ? ld_relaxed64(P.ws.desc1 + (uint64_t)(p0 - i) * k + lane) : FLAG_P;
-        for (int i = 0; i < kLookWin; ++i) {
-          unsigned long long x = v[i];
-          while ((x >> 62) == 0) x = ld_relaxed64(P.ws.desc1 + (uint64_t)(p0 - i) * k + lane);
-          sum += x & VAL_MASK;
-          if ((x >> 62) == 2) {
-            found = 1;
-            break;
-          }
-        }
-      }
-      s_lbsum[w][lane] = sum;
-      s_lbfound[w][lane] = found;
-      __syncthreads();
-      if (w == 0) {
-        if (lane < k && !s_bdone[lane]) {
-          unsigned long long acc = s_acc[lane];
-          for (int w2 = 0; w2 < NW; ++w2) {
-            acc += s_lbsum[w2][lane];
-            if (s_lbfound[w2][lane]) {
-              s_bdone[lane] = 1;
-              break;
-            }
-          }
-          s_acc[lane] = acc;
-        }
-        const bool all = __all_sync(0xffffffffu, lane >= k || s_bdone[lane]);
-        if (lane == 0) s_lbdone = all;
-      }
-      __syncthreads();
-      if (s_lbdone) break;
-      base -= (int64_t)NW * kLookWin;
-    }
-  }
-  if (w == 0) {
-    uint32_t excl = 0, tot = 0, nfrag = 0;
-    if (lane < k) {
-      tot = s_tot[lane];
-      excl = (uint32_t)s_acc[lane];
-      if (t > 0) st_release64(P.ws.desc1 + (uint64_t)t * k + lane, FLAG_P | (excl + tot));
-    }
-    if (lane < k) {
-      const uint32_t jlo = P.divB.div(excl);
-      nfrag = tot ? P.divB.div(excl + tot - 1) - jlo + 1 : 0;
-      s_excl[lane] = excl;
-      s_jlo[lane] = jlo;
-      s_nfrag[lane] = nfrag;
-    }
-    uint32_t incl = nfrag;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += v;
-    }
-    if (lane < k) s_fbase[lane] = incl - nfrag;
-    if (lane == 31) s_nfrag_total = incl;
-    // closings before this tile = sum_b floor(excl_b / B)
-    uint32_t cb = lane < k ? P.divB.div(excl) : 0;
-#pragma unroll
-    for (int o = 16; o; o >>= 1) cb += __shfl_xor_sync(0xffffffffu, cb, o);
-    if (lane == 0) s_closebase = cb;
-  }
-  __syncthreads();
-  for (uint32_t i = tid; i < s_nfrag_total; i += TB) s_slot[i] = 0ull;
   __syncthreads();
 
-  uint32_t rk[IPT], jb[IPT];
+  // global rank, batch, fragment maximum (the IEEE bits of the positive
+  // services order like their values: a max of the high words, then of the
+  // low words among the members holding that high word -- native 32-bit
+  // shared atomics); closings counted per warp
+  uint32_t wclose = 0, cmask = 0;
+  uint32_t fr[PIPT];
 #pragma unroll
-  for (int j = 0; j < IPT; ++j) {
-    rk[j] = 0;
-    jb[j] = 0;
-    if (pb[j]) {
-      const uint32_t b = pb[j] - 1;
-      rk[j] = s_excl[b] + s_woff[w][b] + rl[j];
-      jb[j] = P.divB.div(rk[j]);
-      atomicMax(&s_slot[s_fbase[b] + (jb[j] - s_jlo[b])],
-                (unsigned long long)__double_as_longlong(sv[j]));
+  for (int j = 0; j < PIPT; ++j) {
+    const uint32_t pb = pr[j] & 0xFF;
+    bool closing = false;
+    fr[j] = ~0u;
+    if (pb) {
+      const uint32_t b = pb - 1;
+      const uint32_t rk = s_excl[b] + s_woff[w][b] + (pr[j] >> 8);
+      const uint32_t jb = P.divB.div(rk);
+      fr[j] = s_fbase[b] + (jb - s_jlo[b]);
+      atomicMax(&s_shi[fr[j]], (uint32_t)__double2hiint(sv[j]));
+      closing = rk - jb * B == B - 1;
+      pr[j] = rk;  // from here on: the rank (the bin stays in pbsrc)
+      const uint64_t idx = wbase + j * 32 + lane;
+      P.ws.rank[idx] = rk;
     }
+    cmask |= (uint32_t)closing << j;
+    wclose += __popc(__ballot_sync(0xffffffffu, closing));
   }
+  if (lane == 0) s_wclose[w] = wclose;
   __syncthreads();
-
-  // phase-2 look-back: the open batch's running max carried across tiles.
-  // Tile transform for bin b: f(x) = alpha ? max(x, c) : c.
-  if (w == 0 && lane < k) {
-    const uint32_t excl = s_excl[lane], tot = s_tot[lane];
-    uint32_t alpha;
-    unsigned long long c;
-    if (tot == 0) {
-      alpha = 1;
-      c = 0;
-    } else {
-      const uint32_t jin = s_jlo[lane], end = excl + tot, jout = P.divB.div(end);
-      if (jout == jin) {
-        alpha = 1;
-        c = s_slot[s_fbase[lane]];
-      } else {
-        alpha = 0;
-        c = (end - jout * B) ? s_slot[s_fbase[lane] + s_nfrag[lane] - 1] : 0ull;
-      }
-    }
-    unsigned long long* dv = P.ws.desc2v + (uint64_t)t * k + lane;
-    uint32_t* df = P.ws.desc2f + (uint64_t)t * k + lane;
-    unsigned long long xin = 0, inclv;
-    if (t == 0) {
-      inclv = c;
-      *dv = inclv;
-      __threadfence();
-      st_release32(df, 2);
-    } else {
-      *dv = ((unsigned long long)alpha << 63) | c;
-      __threadfence();
-      st_release32(df, 1);
-      unsigned long long gc = 0;
-      int64_t p = (int64_t)t - 1;
-      while (true) {
-        uint32_t f;
-        do {
-          f = ld_acquire32(P.ws.desc2f + (uint64_t)p * k + lane);
-        } while (f == 0);
-        const unsigned long long v = ld_relaxed64(P.ws.desc2v + (uint64_t)p * k + lane);
-        if (f == 2) {
-          xin = v > gc ? v : gc;
-          break;
-        }
-        const unsigned long long cp = v & ~(1ull << 63);
-        gc = cp > gc ? cp : gc;
-        if (!(v >> 63)) {
-          xin = gc;
-          break;
-        }
-        --p;
-      }
-      inclv = alpha ? (xin > c ? xin : c) : c;
-      *dv = inclv;
-      __threadfence();
-      st_release32(df, 2);
-    }
-    if (tot) {
-      unsigned long long* s0 = &s_slot[s_fbase[lane]];
-      if (xin > *s0) *s0 = xin;
-    }
-    if (t == P.ntiles - 1) {
-      P.ws.fin_cnt[lane] = (unsigned long long)excl + tot;
-      P.ws.fin_open[lane] = inclv;
-    }
+#pragma unroll
+  for (int j = 0; j < PIPT; ++j)
+    if (fr[j] != ~0u && s_shi[fr[j]] == (uint32_t)__double2hiint(sv[j]))
+      atomicMax(&s_slo[fr[j]], (uint32_t)__double2loint(sv[j]));
+  __syncthreads();
+  // fragment maxima into the (bin, batch) slots: one global max per fragment
+  for (uint32_t f = tid; f < s_nfrag_total; f += PT) {
+    uint32_t b = 0;
+    while (b + 1 < k && s_fbase[b + 1] <= f) ++b;
+    atomicMax(P.ws.smax + s_sbase[b] + s_jlo[b] + (f - s_fbase[b]),
+              ((unsigned long long)s_shi[f] << 32) | s_slo[f]);
   }
-  __syncthreads();
-
   // closing records, in closing-request order (dispatch order on the fast path)
-  uint32_t wtot = 0;
-  bool closing[IPT];
-#pragma unroll
-  for (int j = 0; j < IPT; ++j) {
-    closing[j] = pb[j] && (rk[j] - jb[j] * B == B - 1);
-    wtot += __popc(__ballot_sync(0xffffffffu, closing[j]));
-  }
-  if (lane == 0) s_wclose[w] = wtot;
-  __syncthreads();
   uint32_t run = s_closebase;
   for (uint32_t w2 = 0; w2 < w; ++w2) run += s_wclose[w2];
 #pragma unroll
-  for (int j = 0; j < IPT; ++j) {
-    const uint64_t idx = wbase + j * 32 + lane;
-    const uint32_t bal = __ballot_sync(0xffffffffu, closing[j]);
-    if (closing[j]) {
-      const uint32_t q = run + __popc(bal & lanemask_lt());
-      const uint32_t b = pb[j] - 1;
+  for (int j = 0; j < PIPT; ++j) {
+    const bool closing = (cmask >> j) & 1u;
+    const uint32_t bal = __ballot_sync(0xffffffffu, closing);
+    if (closing) {
+      const uint64_t idx = wbase + j * 32 + lane;
+      const uint32_t q = run + __popc(bal & lt);
       P.ws.recR[q] = av[j];
-      P.ws.recS[q] = __longlong_as_double((long long)s_slot[s_fbase[b] + (jb[j] - s_jlo[b])]);
-      P.ws.recBin[q] = (uint8_t)pb[j];
-      P.ws.recJ[q] = jb[j];
+      P.ws.recBin[q] = pbsrc[idx];
+      P.ws.recJ[q] = P.divB.div(pr[j]);
       P.ws.recC[q] = (uint32_t)idx;
     }
     run += __popc(bal);
-    if (idx < n) {
-      P.ws.pb8[idx] = (uint8_t)pb[j];
-      P.ws.rank[idx] = rk[j];
-    }
   }
+}
+
+// the service of batch (bin b+1, j): max over its members (place_kernel)
+__device__ __forceinline__ double batch_service(const WS& ws, uint32_t b, uint32_t j) {
+  return __longlong_as_double((long long)ws.smax[ws.info->sbase[b] + j]);
 }
 
 // Drain partials, batch counts, dispatch-order bases (one warp).
@@ -512,7 +473,6 @@ __global__ void finalize_kernel(WS ws, const double* a, uint32_t n, uint32_t k, 
     if (part) {  // on_drain partial: formed at the last arrival (simulator.hpp:203-205,220)
       const uint32_t q = nclose + (ip - part);
       ws.recR[q] = tmo ? mbw : a[n - 1];  // (or by its timer at W)
-      ws.recS[q] = __longlong_as_double((long long)ws.fin_open[lane]);
       ws.recBin[q] = (uint8_t)(lane + 1);
       ws.recJ[q] = F;
       ws.recC[q] = 0xFFFFFFFFu;
@@ -539,9 +499,10 @@ __global__ void first_arrival_kernel(const uint8_t* __restrict__ pb8, const uint
 }
 
 // Overload: closing index of each bin's first batch (round-0 order key).
-__global__ void ovl_first_kernel(WS ws, uint32_t nclose) {
+__global__ void ovl_first_kernel(WS ws) {
   const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
-  if (q < nclose && ws.recJ[q] == 0) ws.info->cfirst[ws.recBin[q] - 1] = ws.recC[q];
+  if (ws.info->path != 1) return;  // (launched before the host knows the path)
+  if (q < ws.info->nclose && ws.recJ[q] == 0) ws.info->cfirst[ws.recBin[q] - 1] = ws.recC[q];
 }
 
 // Dispatch position of every record + map (bin, j) -> position + member offset.
@@ -552,6 +513,10 @@ __global__ void order_kernel(WS ws, uint32_t* map, uint32_t* order, uint32_t* df
   const Info* I = ws.info;
   const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= I->nb) return;
+  if (path < 0) {  // the device's own path (path 2 starts from closing order)
+    path = I->path == 2 ? 0 : (int32_t)I->path;
+    if (path == 3) return;
+  }
   const uint32_t b = ws.recBin[q] - 1, j = ws.recJ[q];
   const bool partial = q >= I->nclose;
   uint32_t pos;
@@ -604,7 +569,8 @@ __global__ void order_kernel(WS ws, uint32_t* map, uint32_t* order, uint32_t* df
 
 // groups of more than B equal arrivals: (start, end) pairs, any order
 __global__ void tie_groups_kernel(const double* __restrict__ a, uint32_t n, uint32_t B, uint2* groups,
-                                  uint32_t* ngroups) {
+                                  uint32_t* ngroups, const Info* I) {
+  if (I->path != 2) return;  // (launched before the host knows the path)
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const double v = a[i];
     if (i > 0 && a[i - 1] == v) continue;
@@ -622,7 +588,7 @@ __global__ void tie_groups_kernel(const double* __restrict__ a, uint32_t n, uint
 struct TieArgs {
   const uint2* groups;
   const uint32_t* ngroups;
-  const unsigned long long* desc1;  // partition look-back: inclusive per-tile bin counts
+  uint32_t ntiles;                  // partition tiles (WS::tcount: exclusive tile prefixes)
   WS ws;
   uint32_t *map, *order, *dfirst;
   uint32_t n, k, B;
@@ -642,13 +608,14 @@ __global__ void __launch_bounds__(256) tie_order_kernel(TieArgs T) {
     __syncthreads();
     if (tid < 32) s_c[0][tid] = s_c[1][tid] = 0;
     __syncthreads();
-    // count_b[0, x) = inclusive count of the previous tile + this tile's head
+    // count_b[0, x) = the tile's exclusive prefix + this tile's head
 #pragma unroll
     for (int side = 0; side < 2; ++side) {
       const uint32_t x = side ? G.y : G.x;
-      const uint32_t t = x / TILE;
-      if (tid < k && t > 0) atomicAdd(&s_c[side][tid], (uint32_t)(T.desc1[(uint64_t)(t - 1) * k + tid] & VAL_MASK));
-      for (uint32_t i = t * TILE + tid; i < x; i += blockDim.x) atomicAdd(&s_c[side][T.ws.pb8[i] - 1], 1u);
+      const uint32_t t = x / PTILE;
+      if (tid < k)
+        atomicAdd(&s_c[side][tid], t < T.ntiles ? T.ws.tcount[(uint64_t)tid * T.ntiles + t] : (uint32_t)T.ws.fin_cnt[tid]);
+      for (uint32_t i = t * PTILE + tid; i < x; i += blockDim.x) atomicAdd(&s_c[side][T.ws.pb8[i] - 1], 1u);
     }
     __syncthreads();
     if (tid < 32) {
@@ -729,9 +696,10 @@ __global__ void gather_kernel(WS ws, const uint32_t* order, int32_t path, uint32
   const Info* I = ws.info;
   const uint32_t d = blockIdx.x * blockDim.x + threadIdx.x;
   if (d >= I->nb) return;
+  if (path < 0) path = (int32_t)I->path;
   const uint32_t q = path == 0 ? d : order[d];
   dR[d] = ws.recR[q];
-  dS[d] = ws.recS[q];
+  dS[d] = batch_service(ws, ws.recBin[q] - 1, ws.recJ[q]);
   const uint8_t b = ws.recBin[q];
   if (dBin) dBin[d] = b;
   if (dSize) dSize[d] = q < I->nclose ? B : I->rem[b - 1];
@@ -741,7 +709,7 @@ __global__ void gather_kernel(WS ws, const uint32_t* order, int32_t path, uint32
 struct LArgs {
   const double* R;
   const double* S;
-  uint32_t nb;
+  const uint32_t* nbp;  // batch count (device: known after the partition)
   uint8_t* split;   // 1 = certified idle start, 2 = ambiguous, 0 = certified busy
   double* Dt;       // approximate D after each batch (binade prediction)
   double* busy_part;
@@ -813,13 +781,15 @@ __global__ void __launch_bounds__(LB) lindley_scan_kernel(LArgs L) {
   if (tid == 0) s_blk = atomicAdd(L.counter, 1u);
   __syncthreads();
   const uint32_t blk = s_blk;
+  const uint32_t nb = *L.nbp;
+  if ((uint64_t)blk * LTILE >= nb) return;  // grid sized for the upper bound
   const uint64_t d0 = (uint64_t)blk * LTILE + tid * LI;
   double R[LI], S[LI];
   MP f{0.0, -CUDART_INF};
   double bs = 0.0;
 #pragma unroll
   for (int i = 0; i < LI; ++i) {
-    const bool v = d0 + i < L.nb;
+    const bool v = d0 + i < nb;
     R[i] = v ? L.R[d0 + i] : -CUDART_INF;
     S[i] = v ? L.S[d0 + i] : 0.0;
     f = compose(f, MP{S[i], R[i] + S[i]});
@@ -886,7 +856,7 @@ __global__ void __launch_bounds__(LB) lindley_scan_kernel(LArgs L) {
   double Dp = pre.C;  // applied to D_{-1} = -inf (server idle before the first batch)
 #pragma unroll
   for (int i = 0; i < LI; ++i) {
-    if (d0 + i < L.nb) {
+    if (d0 + i < nb) {
       uint8_t code;
       if (Dp == -CUDART_INF) {
         code = kSplit;
@@ -903,10 +873,11 @@ __global__ void __launch_bounds__(LB) lindley_scan_kernel(LArgs L) {
 
 // Exact serial recurrence inside every certified busy period.
 __global__ void lindley_segments_kernel(const double* __restrict__ R, const double* __restrict__ S,
-                                        const uint8_t* __restrict__ split, uint32_t nb,
+                                        const uint8_t* __restrict__ split, const uint32_t* nbp,
                                         double* __restrict__ start, double* __restrict__ finish,
                                         const int* __restrict__ bad) {
   if (!*bad) return;  // fallback only: the binade scan produced exact values
+  const uint32_t nb = *nbp;
   const uint32_t d = blockIdx.x * blockDim.x + threadIdx.x;
   if (d >= nb || split[d] != kSplit) return;
   double D = __dadd_rn(R[d], S[d]);  // idle server: start = formation time
@@ -982,7 +953,7 @@ struct BArgs {
   const double* S;
   const double* Dt;
   const uint8_t* code;
-  uint32_t nb;
+  const uint32_t* nbp;  // batch count (device)
   double tol_rel;
   long long* p0;       // prefix map per batch (within its run)
   long long* p1;
@@ -1032,6 +1003,8 @@ __global__ void __launch_bounds__(LB) binade_scan_kernel(BArgs A) {
   if (tid == 0) s_blk = atomicAdd(A.counter, 1u);
   __syncthreads();
   const uint32_t blk = s_blk;
+  const uint32_t nb = *A.nbp;
+  if ((uint64_t)blk * LTILE >= nb) return;  // grid sized for the upper bound
   const uint64_t d0 = (uint64_t)blk * LTILE + tid * LI;
   SegV v[LI];
   SegV acc{{0, 0}, 0, 0};
@@ -1039,7 +1012,7 @@ __global__ void __launch_bounds__(LB) binade_scan_kernel(BArgs A) {
   for (int i = 0; i < LI; ++i) {
     const uint64_t d = d0 + i;
     SegV e{{0, 0}, 0, 0};
-    if (d < A.nb) {
+    if (d < nb) {
       const double dcur = A.Dt[d];
       const double dprev = d ? A.Dt[d - 1] : -1.0;
       if (run_head(A.code[d], dprev, dcur, A.tol_rel)) {
@@ -1113,13 +1086,13 @@ __global__ void __launch_bounds__(LB) binade_scan_kernel(BArgs A) {
 #pragma unroll
   for (int i = 0; i < LI; ++i) {
     const uint64_t d = d0 + i;
-    if (d >= A.nb) break;
+    if (d >= nb) break;
     const SegV r = scomb(pre, v[i]);
     A.p0[d] = r.m.i0;
     A.p1[d] = r.m.i1;
     const uint32_t h = r.hp - 1;  // batch 0 is always a head
     A.head_of[d] = h;
-    bool last = d + 1 == A.nb;
+    bool last = d + 1 == nb;
     if (!last) last = run_head(A.code[d + 1], A.Dt[d], A.Dt[d + 1], A.tol_rel);
     if (last) A.run_last[h] = (uint32_t)d;
   }
@@ -1144,9 +1117,10 @@ __device__ __forceinline__ double run_end(double Dh, uint32_t h, uint32_t last, 
 __global__ void binade_chain_kernel(const double* __restrict__ R, const double* __restrict__ S,
                                     const double* __restrict__ Dt, const uint8_t* __restrict__ code,
                                     const long long* __restrict__ p0, const long long* __restrict__ p1,
-                                    const uint32_t* __restrict__ run_last, uint32_t nb,
+                                    const uint32_t* __restrict__ run_last, const uint32_t* nbp,
                                     double* __restrict__ start, double* __restrict__ finish,
                                     int* bad) {
+  const uint32_t nb = *nbp;
   const uint32_t d = blockIdx.x * blockDim.x + threadIdx.x;
   if (d >= nb || code[d] != kSplit) return;
   uint32_t h = d;
@@ -1170,8 +1144,9 @@ __global__ void binade_chain_kernel(const double* __restrict__ R, const double* 
 __global__ void binade_fill_kernel(const double* __restrict__ S, const double* __restrict__ Dt,
                                    const uint8_t* __restrict__ code, const long long* __restrict__ p0,
                                    const long long* __restrict__ p1, const uint32_t* __restrict__ head_of,
-                                   uint32_t nb, double tol_rel, double* __restrict__ start,
+                                   const uint32_t* nbp, double tol_rel, double* __restrict__ start,
                                    double* __restrict__ finish, int* bad) {
+  const uint32_t nb = *nbp;
   const uint32_t d = blockIdx.x * blockDim.x + threadIdx.x;
   if (d >= nb) return;
   const double dprev = d ? Dt[d - 1] : -1.0;
@@ -1223,7 +1198,7 @@ struct QArgs {
 // last_completion_ accumulate in dispatch order, as the reference does.
 constexpr uint32_t KW_CH = 1024, KW_HEAP = 2048;
 __global__ void __launch_bounds__(256) kw_dispatch_kernel(const double* __restrict__ R,
-                                                          const double* __restrict__ S, uint32_t nb,
+                                                          const double* __restrict__ S, const uint32_t* nbp,
                                                           uint32_t nsrv, double* heap_g,
                                                           double* __restrict__ start,
                                                           double* __restrict__ finish,
@@ -1231,6 +1206,7 @@ __global__ void __launch_bounds__(256) kw_dispatch_kernel(const double* __restri
   __shared__ double sA[KW_CH], sB[KW_CH];  // (R, S) in, (start, finish) out
   __shared__ double sheap[KW_HEAP];
   double* heap = nsrv <= KW_HEAP ? sheap : heap_g;
+  const uint32_t nb = *nbp;
   for (uint32_t i = threadIdx.x; i < nsrv; i += blockDim.x) heap[i] = -CUDART_INF;  // all idle
   double busy = 0.0, last = 0.0;
   for (uint32_t base = 0; base < nb; base += KW_CH) {
@@ -1275,42 +1251,65 @@ __global__ void __launch_bounds__(256) kw_dispatch_kernel(const double* __restri
   }
 }
 
-__global__ void __launch_bounds__(256) request_kernel(QArgs Q) {
-  __shared__ double s_sum[8];
-  __shared__ unsigned long long s_min[8], s_max[8];
-  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+constexpr int RQ_T = 256, RQ_E = 4;  // request pass: threads, requests per thread
+__global__ void __launch_bounds__(RQ_T) request_kernel(QArgs Q) {
+  __shared__ double s_sum[RQ_T / 32];
+  __shared__ unsigned long long s_min[RQ_T / 32], s_max[RQ_T / 32];
+  __shared__ uint32_t s_nbat[BB_TRACE_MAX_BINS], s_base[BB_TRACE_MAX_BINS];
   const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (threadIdx.x < BB_TRACE_MAX_BINS) {
+    s_nbat[threadIdx.x] = Q.info->nbat[threadIdx.x];
+    s_base[threadIdx.x] = Q.info->bin_base[threadIdx.x];
+  }
+  __syncthreads();
+  const uint64_t base = (uint64_t)blockIdx.x * (RQ_T * RQ_E) + threadIdx.x;
+  uint32_t bin[RQ_E], rk[RQ_E], d[RQ_E];
+  double a[RQ_E], comp[RQ_E];
+  // every load of a stage in flight before the next stage uses it
+#pragma unroll
+  for (int e = 0; e < RQ_E; ++e) {
+    const uint64_t i = base + e * RQ_T;
+    const bool v = i < Q.n;
+    bin[e] = v ? Q.pb8[i] : 0u;
+    rk[e] = v ? Q.rank[i] : 0u;
+    a[e] = v ? Q.a[i] : 0.0;
+  }
+#pragma unroll
+  for (int e = 0; e < RQ_E; ++e) {
+    d[e] = BB_NO_BATCH;
+    if (bin[e]) {
+      const uint32_t j = Q.divB.div(rk[e]);
+      if (j < s_nbat[bin[e] - 1]) d[e] = Q.map[s_base[bin[e] - 1] + j];
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < RQ_E; ++e) comp[e] = d[e] != BB_NO_BATCH ? Q.finish[d[e]] : BB_QNAN;
   double lat = 0.0;
   unsigned long long kmin = KEY_UNSERVED, kmax = 0;
-  if (i < Q.n) {
-    const uint32_t b = Q.pb8[i];
+#pragma unroll
+  for (int e = 0; e < RQ_E; ++e) {
+    const uint64_t i = base + e * RQ_T;
+    if (i >= Q.n) continue;
     unsigned long long key = KEY_UNSERVED;
-    double comp = BB_QNAN;
-    uint32_t bid = BB_NO_BATCH;
-    if (b) {
-      const uint32_t r = Q.rank[i];
-      const uint32_t j = Q.divB.div(r);
-      if (j < Q.info->nbat[b - 1]) {
-        const uint32_t d = Q.map[Q.info->bin_base[b - 1] + j];
-        comp = Q.finish[d];
-        lat = __dsub_rn(comp, Q.a[i]);  // simulator.hpp:294
-        key = (unsigned long long)__double_as_longlong(lat);
-        kmin = kmax = key;
-        bid = d;
-        if (Q.members) Q.members[Q.dfirst[d] + (r - j * Q.B)] = i;
-      }
+    if (d[e] != BB_NO_BATCH) {
+      const double x = __dsub_rn(comp[e], a[e]);  // simulator.hpp:294
+      lat += x;
+      key = (unsigned long long)__double_as_longlong(x);
+      kmin = key < kmin ? key : kmin;
+      kmax = key > kmax ? key : kmax;
+      if (Q.members) Q.members[Q.dfirst[d[e]] + (rk[e] - Q.divB.div(rk[e]) * Q.B)] = (uint32_t)i;
     }
     Q.key[i] = key;
-    if (Q.completion) Q.completion[i] = comp;
-    if (Q.batch) Q.batch[i] = bid;
+    if (Q.completion) Q.completion[i] = comp[e];
+    if (Q.batch) Q.batch[i] = d[e];
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
     lat += __shfl_xor_sync(0xffffffffu, lat, o);
-    const unsigned long long a = __shfl_xor_sync(0xffffffffu, kmin, o);
-    const unsigned long long b = __shfl_xor_sync(0xffffffffu, kmax, o);
-    kmin = a < kmin ? a : kmin;
-    kmax = b > kmax ? b : kmax;
+    const unsigned long long x = __shfl_xor_sync(0xffffffffu, kmin, o);
+    const unsigned long long y = __shfl_xor_sync(0xffffffffu, kmax, o);
+    kmin = x < kmin ? x : kmin;
+    kmax = y > kmax ? y : kmax;
   }
   if (lane == 0) {
     s_sum[w] = lat;
@@ -1319,13 +1318,13 @@ __global__ void __launch_bounds__(256) request_kernel(QArgs Q) {
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    double s = 0.0;
-    for (int q = 0; q < 8; ++q) {
-      s += s_sum[q];
+    double sum = 0.0;
+    for (int q = 0; q < RQ_T / 32; ++q) {
+      sum += s_sum[q];
       kmin = s_min[q] < kmin ? s_min[q] : kmin;
       kmax = s_max[q] > kmax ? s_max[q] : kmax;
     }
-    Q.lat_part[blockIdx.x] = s;
+    Q.lat_part[blockIdx.x] = sum;
     if (kmin != KEY_UNSERVED) {
       atomicMin(&Q.kminmax[0], kmin);
       atomicMax(&Q.kminmax[1], kmax);
@@ -1334,8 +1333,10 @@ __global__ void __launch_bounds__(256) request_kernel(QArgs Q) {
 }
 
 // deterministic sum of block partials (one block)
-__global__ void sum_kernel(const double* part, uint32_t m, double* out) {
+// nbp: m = the Lindley tiles of *nbp batches (device count)
+__global__ void sum_kernel(const double* part, uint32_t m, double* out, const uint32_t* nbp = nullptr) {
   __shared__ double s[256];
+  if (nbp) m = (*nbp + LTILE - 1) / LTILE;
   double acc = 0.0;
   for (uint32_t i = threadIdx.x; i < m; i += 256) acc += part[i];
   s[threadIdx.x] = acc;
@@ -1347,17 +1348,43 @@ __global__ void sum_kernel(const double* part, uint32_t m, double* out) {
   if (threadIdx.x == 0) *out = s[0];
 }
 
+// the run's last completion (simulator.hpp:275; one server: the last batch's
+// finish) and first arrival, for makespan = last - a[0] (:284-285)
+__global__ void scalars_kernel(const Info* I, const double* finish, const double* last_ms,
+                               const double* a, double* out) {
+  const uint32_t nb = I->nb;
+  out[0] = last_ms ? *last_ms : (nb ? finish[nb - 1] : 0.0);
+  out[1] = a[0];
+}
+
 // --------------------------------------------------------------- selection
+// Visit every key, four per thread per step (two 16-byte loads in flight).
+template <class F>
+__device__ __forceinline__ void for_keys(const unsigned long long* __restrict__ key, uint32_t m, F&& f) {
+  const uint64_t step = (uint64_t)gridDim.x * blockDim.x * 4;
+  for (uint64_t i = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4; i < m; i += step) {
+    if (i + 4 <= m) {
+      const ulonglong2 x = *reinterpret_cast<const ulonglong2*>(key + i);
+      const ulonglong2 y = *reinterpret_cast<const ulonglong2*>(key + i + 2);
+      f(x.x);
+      f(x.y);
+      f(y.x);
+      f(y.y);
+    } else {
+      for (uint64_t q = i; q < m; ++q) f(key[q]);
+    }
+  }
+}
+
 __global__ void hist_kernel(const unsigned long long* __restrict__ key, uint32_t m,
                             unsigned long long lo, unsigned long long hi, uint32_t shift,
                             uint32_t* __restrict__ hist) {
   __shared__ uint32_t h[HBINS];
   for (int i = threadIdx.x; i < HBINS; i += blockDim.x) h[i] = 0;
   __syncthreads();
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
-    const unsigned long long v = key[i];
+  for_keys(key, m, [&](unsigned long long v) {
     if (v >= lo && v <= hi) atomicAdd(&h[(uint32_t)((v - lo) >> shift)], 1u);
-  }
+  });
   __syncthreads();
   for (int i = threadIdx.x; i < HBINS; i += blockDim.x)
     if (h[i]) atomicAdd(&hist[i], h[i]);
@@ -1388,7 +1415,21 @@ struct SelState {
   uint32_t bucket[kSelMax];
 };
 
-__global__ void sel_init_kernel(SelState* S, const unsigned long long* kminmax) {
+// interpolated_quantile's ranks (binning.hpp:98-104) from the completed count
+// (pos = q (n-1) rounded as on the host, no contraction), then the range
+__global__ void sel_init_kernel(SelState* S, const unsigned long long* kminmax, const Info* I) {
+  const unsigned long long nc = I->nc;
+  uint32_t nt = 0;
+  if (nc > 0) {
+    const double qs[2] = {0.50, 0.99};
+    for (int q = 0; q < 2; ++q) {
+      const double pos = __dmul_rn(qs[q], (double)(nc - 1));
+      const unsigned long long idx = (unsigned long long)pos;
+      S->rank[nt++] = idx;
+      if (idx + 1 < nc) S->rank[nt++] = idx + 1;
+    }
+  }
+  S->nt = nt;
   const unsigned long long lo = kminmax[0], hi = kminmax[1];
   S->base = lo;
   S->top = hi;
@@ -1406,10 +1447,9 @@ __global__ void sel_hist_kernel(const unsigned long long* __restrict__ key, uint
   __syncthreads();
   const unsigned long long lo = S->base, hi = S->top;
   const uint32_t shift = S->shift;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
-    const unsigned long long v = key[i];
+  for_keys(key, m, [&](unsigned long long v) {
     if (v >= lo && v <= hi) atomicAdd(&h[(uint32_t)((v - lo) >> shift)], 1u);
-  }
+  });
   __syncthreads();
   for (int i = threadIdx.x; i < HBINS; i += blockDim.x)
     if (h[i]) atomicAdd(&hist[i], h[i]);
@@ -1528,12 +1568,11 @@ __global__ void sel_hist2_kernel(const unsigned long long* __restrict__ key, uin
   }
   __syncthreads();
   if (!S->need_collect) return;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
-    const unsigned long long v = key[i];
+  for_keys(key, m, [&](unsigned long long v) {
 #pragma unroll
     for (int q = 0; q < kSelMax; ++q)
       if (v >= s_lo[q] && v <= s_hi[q]) atomicAdd(&h[q][(uint32_t)((v - s_lo[q]) >> s_sh[q])], 1u);
-  }
+  });
   __syncthreads();
   for (int i = threadIdx.x; i < kSelMax * kSub; i += blockDim.x)
     if ((&h[0][0])[i]) atomicAdd(&hist2[i], (&h[0][0])[i]);
@@ -1587,8 +1626,7 @@ __global__ void sel_collect_kernel(const unsigned long long* __restrict__ key, u
     lo[q] = q < nt ? S->lo[q] : 1;
     hi[q] = q < nt && S->lo[q] != S->hi[q] ? S->hi[q] : 0;
   }
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
-    const unsigned long long v = key[i];
+  for_keys(key, m, [&](unsigned long long v) {
     bool in = false;
 #pragma unroll
     for (int q = 0; q < kSelMax; ++q) in |= v >= lo[q] && v <= hi[q];
@@ -1596,7 +1634,7 @@ __global__ void sel_collect_kernel(const unsigned long long* __restrict__ key, u
       const uint32_t slot = atomicAdd(&S->ncand, 1u);
       if (slot < cap) out[slot] = v;
     }
-  }
+  });
 }
 
 // refine every unresolved target on the candidates, all levels in smem
@@ -1933,7 +1971,7 @@ void trace_run(const TraceArgs& A, TraceResult* R, cudaStream_t s) {
   Pool pool;
   pool.s = s;
   const uint32_t n = A.n, k = A.k, B = A.B;
-  const uint32_t ntiles = (n + TILE - 1) / TILE;
+  const uint32_t ntiles = (n + PTILE - 1) / PTILE;
   const uint64_t rec_cap = (uint64_t)n / B + k + 1;
   WS ws{};
   Info info{};
@@ -1944,32 +1982,58 @@ void trace_run(const TraceArgs& A, TraceResult* R, cudaStream_t s) {
   uint8_t *dbin = nullptr, *split = nullptr;
   bool tm = false;   // max_batch_wait timer path
   bool tmo = false;  // overload without flush, with timers: partials at W
-  unsigned long long nc_run = 0;
+  unsigned long long nc_run = 0, tm_nc = 0;
+  uint32_t tm_counts[1] = {0};
+  // the partition's verdict: a request error, or non-monotone arrivals
+  auto input_error = [&]() -> bool {
+    if (herr.packed != ~0ull) {
+      const unsigned long long idx = herr.packed >> 8;
+      const int code = (int)(herr.packed & 0xFF);
+      R->status = code;
+      if (code == BB_EDOMAIN && herr.aux == 1)
+        snprintf(R->message, sizeof R->message, "simulation: drew a non-positive service time");
+      else if (code == BB_EDOMAIN)
+        snprintf(R->message, sizeof R->message, "assign_bin: length %.17g outside bin support",
+                 herr.value);
+      else
+        snprintf(R->message, sizeof R->message, "request %llu: predicted bin %g out of range", idx,
+                 herr.value);
+      return true;
+    }
+    if (info.path == 3) {
+      R->status = BB_EINVAL;
+      snprintf(R->message, sizeof R->message, "trace arrays: arrivals must be non-decreasing");
+      return true;
+    }
+    return false;
+  };
+  // Without max_batch_wait the pipeline runs to the end with no host round
+  // trip: buffers are sized for the batch-count bound n/B + k + 1 and the
+  // kernels read the batch count, path and completed count from the device.
+  // Timers order their batches on the host (below): one sync here.
+  const bool host_sync = A.max_batch_wait > 0;
+
   uint32_t *tm_list = nullptr, *tm_off = nullptr, *tm_segj = nullptr, *tm_recP = nullptr;
   BB_CK(cudaEventCreate(&ev0));
   BB_CK(cudaEventCreate(&ev1));
   BB_CK(cudaEventCreate(&ev2));
   BB_CK(pool.alloc((void**)&ws.counters, 16));
-  BB_CK(pool.alloc((void**)&ws.desc1, (size_t)ntiles * k * 8));
-  BB_CK(pool.alloc((void**)&ws.desc2v, (size_t)ntiles * k * 8));
-  BB_CK(pool.alloc((void**)&ws.desc2f, (size_t)ntiles * k * 4));
-  BB_CK(pool.alloc((void**)&ws.pb8, n));
+  BB_CK(pool.alloc((void**)&ws.tcount, (size_t)ntiles * k * 4));
+  BB_CK(pool.alloc((void**)&ws.smax, (rec_cap + 32) * 8));
+  if (A.pred) ws.pb8 = const_cast<uint8_t*>(A.pred);  // given predictions are read in place
+  else BB_CK(pool.alloc((void**)&ws.pb8, n));
   BB_CK(pool.alloc((void**)&ws.rank, (size_t)n * 4));
   BB_CK(pool.alloc((void**)&ws.recR, rec_cap * 8));
-  BB_CK(pool.alloc((void**)&ws.recS, rec_cap * 8));
   BB_CK(pool.alloc((void**)&ws.recBin, rec_cap));
   BB_CK(pool.alloc((void**)&ws.recJ, rec_cap * 4));
   BB_CK(pool.alloc((void**)&ws.recC, rec_cap * 4));
   BB_CK(pool.alloc((void**)&ws.fin_cnt, 32 * 8));
-  BB_CK(pool.alloc((void**)&ws.fin_open, 32 * 8));
   BB_CK(pool.alloc((void**)&ws.flags, 4));
   BB_CK(pool.alloc((void**)&ws.err, sizeof(DevError)));
   BB_CK(pool.alloc((void**)&ws.info, sizeof(Info)));
   BB_CK(cudaMemsetAsync(ws.counters, 0, 16, s));
-  BB_CK(cudaMemsetAsync(ws.desc1, 0, (size_t)ntiles * k * 8, s));
-  BB_CK(cudaMemsetAsync(ws.desc2f, 0, (size_t)ntiles * k * 4, s));
   BB_CK(cudaMemsetAsync(ws.fin_cnt, 0, 32 * 8, s));
-  BB_CK(cudaMemsetAsync(ws.fin_open, 0, 32 * 8, s));
+  BB_CK(cudaMemsetAsync(ws.smax, 0, (rec_cap + 32) * 8, s));
   BB_CK(cudaMemsetAsync(ws.flags, 0, 4, s));
   BB_CK(cudaMemsetAsync(ws.err, 0xFF, 8, s));
   BB_CK(cudaEventRecord(ev0, s));
@@ -1991,38 +2055,27 @@ void trace_run(const TraceArgs& A, TraceResult* R, cudaStream_t s) {
     P.one_minus_p = 1.0 - A.p_error;
     P.divB = FastDiv(B);
     P.ws = ws;
-    partition_kernel<<<ntiles, TB, 0, s>>>(P);
-    note_launch();
+    count_kernel<<<ntiles, PT, 0, s>>>(P);
+    tscan_kernel<<<k, TS_T, 0, s>>>(ws, ntiles, k, B);
+    sbase_kernel<<<1, 1, 0, s>>>(ws, k, B);
+    if (P.pred && P.tb_out) place_kernel<true><<<ntiles, PT, 0, s>>>(P);
+    else place_kernel<false><<<ntiles, PT, 0, s>>>(P);
+    note_launch(4);
     BB_CK(cudaGetLastError());
   }
   BB_CK(cudaEventRecord(ev1, s));
-  if (A.req_pred_bin) BB_CK(cudaMemcpyAsync(A.req_pred_bin, ws.pb8, n, cudaMemcpyDeviceToDevice, s));
+  if (A.req_pred_bin && A.req_pred_bin != ws.pb8)
+    BB_CK(cudaMemcpyAsync(A.req_pred_bin, ws.pb8, n, cudaMemcpyDeviceToDevice, s));
   finalize_kernel<<<1, 32, 0, s>>>(ws, A.a, n, k, B, A.flush, A.max_batch_wait);
   note_launch();
   BB_CK(cudaGetLastError());
-  BB_CK(cudaMemcpyAsync(&info, ws.info, sizeof(Info), cudaMemcpyDeviceToHost, s));
-  BB_CK(cudaMemcpyAsync(&herr, ws.err, sizeof(DevError), cudaMemcpyDeviceToHost, s));
-  BB_CK(cudaStreamSynchronize(s));
-  if (herr.packed != ~0ull) {
-    const unsigned long long idx = herr.packed >> 8;
-    const int code = (int)(herr.packed & 0xFF);
-    R->status = code;
-    if (code == BB_EDOMAIN && herr.aux == 1)
-      snprintf(R->message, sizeof R->message, "simulation: drew a non-positive service time");
-    else if (code == BB_EDOMAIN)
-      snprintf(R->message, sizeof R->message, "assign_bin: length %.17g outside bin support",
-               herr.value);
-    else
-      snprintf(R->message, sizeof R->message, "request %llu: predicted bin %g out of range", idx,
-               herr.value);
-    goto cleanup;
+  if (host_sync) {
+    BB_CK(cudaMemcpyAsync(&info, ws.info, sizeof(Info), cudaMemcpyDeviceToHost, s));
+    BB_CK(cudaMemcpyAsync(&herr, ws.err, sizeof(DevError), cudaMemcpyDeviceToHost, s));
+    BB_CK(cudaStreamSynchronize(s));
+    if (input_error()) goto cleanup;
+    R->path = (int32_t)info.path;
   }
-  if (info.path == 3) {
-    R->status = BB_EINVAL;
-    snprintf(R->message, sizeof R->message, "trace arrays: arrivals must be non-decreasing");
-    goto cleanup;
-  }
-  R->path = (int32_t)info.path;
   // max_batch_wait: overload with flush drains every bin at t = 0, so the
   // timers go stale and the plain pipeline applies; otherwise the timer path
   tm = A.max_batch_wait > 0 && info.path != 1;
@@ -2035,7 +2088,7 @@ void trace_run(const TraceArgs& A, TraceResult* R, cudaStream_t s) {
     std::vector<uint32_t> fa(k, 0);
     BB_CK(pool.alloc((void**)&dfa, (size_t)k * 4));
     BB_CK(cudaMemsetAsync(dfa, 0, (size_t)k * 4, s));
-    if (info.nclose) ovl_first_kernel<<<grid_for(info.nclose, 256), 256, 0, s>>>(ws, info.nclose);
+    if (info.nclose) ovl_first_kernel<<<grid_for(info.nclose, 256), 256, 0, s>>>(ws);
     first_arrival_kernel<<<grid_for(n, 256), 256, 0, s>>>(ws.pb8, ws.rank, n, dfa);
     note_launch(2);
     BB_CK(cudaGetLastError());
@@ -2086,7 +2139,7 @@ void trace_run(const TraceArgs& A, TraceResult* R, cudaStream_t s) {
     }
   }
   {
-    uint32_t nb = info.nb;
+    uint32_t nb = host_sync ? info.nb : (uint32_t)rec_cap;  // (without sync: the bound; grids and buffers)
     if (tm) {  // ---- timer path: per-bin segmentation, sort by formation
       std::vector<uint32_t> hoff(k), hcnt(k), hn(k);
       uint32_t acc = 0;
@@ -2190,6 +2243,11 @@ void trace_run(const TraceArgs& A, TraceResult* R, cudaStream_t s) {
       tm_segj = segj;
       tm_recP = recP;
       nc_run = n;  // every request completes: drained, or formed by its timer
+      // the kernels below read the batch and completed counts on the device
+      tm_counts[0] = nb;
+      tm_nc = nc_run;
+      BB_CK(cudaMemcpyAsync(&ws.info->nb, &tm_counts[0], 4, cudaMemcpyHostToDevice, s));
+      BB_CK(cudaMemcpyAsync(&ws.info->nc, &tm_nc, 8, cudaMemcpyHostToDevice, s));
     } else {
       BB_CK(pool.alloc((void**)&map, (size_t)nb * 4 + 4));
       BB_CK(pool.alloc((void**)&order, (size_t)nb * 4 + 4));
@@ -2197,31 +2255,29 @@ void trace_run(const TraceArgs& A, TraceResult* R, cudaStream_t s) {
       BB_CK(pool.alloc((void**)&dR, (size_t)nb * 8 + 8));
       BB_CK(pool.alloc((void**)&dS, (size_t)nb * 8 + 8));
       BB_CK(pool.alloc((void**)&split, nb + 1));
-      for (uint32_t b = 0; b < k; ++b) R->per_bin[b] = info.nbat[b];
-      nc_run = info.nc;
     }
-    R->n_batches = nb;
-    R->n_completed = nc_run;
+    const uint32_t* nbp = &ws.info->nb;
     // nb == 0 (nothing served, finish() :283) still runs the request pass so
     // every request reports kNoBatch / NaN completion
     start = A.bat_start;
     finish = A.bat_finish;
     if (!start) BB_CK(pool.alloc((void**)&start, (size_t)nb * 8 + 8));
     if (!finish) BB_CK(pool.alloc((void**)&finish, (size_t)nb * 8 + 8));
-    if (!tm && !tmo && info.path == 1 && info.nclose) {
-      ovl_first_kernel<<<grid_for(info.nclose, 256), 256, 0, s>>>(ws, info.nclose);
+    if (!tm && !tmo && nb) {  // overload: first closings (a no-op on the other paths)
+      ovl_first_kernel<<<grid_for(nb, 256), 256, 0, s>>>(ws);
       note_launch();
       BB_CK(cudaGetLastError());
     }
     if (!tm) {
       // path 2 (tie groups of more than B at finite times): closing order
       // first, then each such group re-orders its own range of records
-      const int32_t opath = info.path == 2 ? 0 : (int32_t)info.path;
+      // (the device's path unless the host synchronised)
+      const int32_t opath = !host_sync ? -1 : info.path == 2 ? 0 : (int32_t)info.path;
       if (nb) order_kernel<<<grid_for(nb, 256), 256, 0, s>>>(ws, map, order, dfirst, k, B, A.flush,
                                                      opath, (int32_t)tmo);
       note_launch();
       BB_CK(cudaGetLastError());
-      if (info.path == 2 && nb) {
+      if ((!host_sync || info.path == 2) && nb) {
         const uint32_t gcap = n / (B + 1) + 1;
         uint2* groups;
         uint32_t* ngroups;
@@ -2232,14 +2288,14 @@ void trace_run(const TraceArgs& A, TraceResult* R, cudaStream_t s) {
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         tie_groups_kernel<<<std::min<uint32_t>(grid_for(n, 256), sms * 8), 256, 0, s>>>(A.a, n, B, groups,
-                                                                                      ngroups);
-        TieArgs T{groups, ngroups, ws.desc1, ws, map, order, dfirst, n, k, B, A.flush};
+                                                                                      ngroups, ws.info);
+        TieArgs T{groups, ngroups, ntiles, ws, map, order, dfirst, n, k, B, A.flush};
         tie_order_kernel<<<std::min<uint32_t>(gcap, sms * 4), 256, 0, s>>>(T);
         note_launch(2);
         BB_CK(cudaGetLastError());
       }
-      if (nb) gather_kernel<<<grid_for(nb, 256), 256, 0, s>>>(ws, order, (int32_t)info.path, B, dR, dS,
-                                                      A.bat_bin, A.bat_size);
+      if (nb) gather_kernel<<<grid_for(nb, 256), 256, 0, s>>>(ws, order, host_sync ? (int32_t)info.path : -1,
+                                                      B, dR, dS, A.bat_bin, A.bat_size);
       note_launch();
       BB_CK(cudaGetLastError());
     }
@@ -2250,7 +2306,7 @@ void trace_run(const TraceArgs& A, TraceResult* R, cudaStream_t s) {
     if (A.n_servers > 1) {  // S servers: Kiefer-Wolfowitz, dispatch order
       double* heap_g = nullptr;
       if (A.n_servers > KW_HEAP) BB_CK(pool.alloc((void**)&heap_g, (size_t)A.n_servers * 8));
-      kw_dispatch_kernel<<<1, 256, 0, s>>>(dR, dS, nb, A.n_servers, heap_g, start, finish, busy_sum,
+      kw_dispatch_kernel<<<1, 256, 0, s>>>(dR, dS, nbp, A.n_servers, heap_g, start, finish, busy_sum,
                                            last_dev);
       note_launch();
       BB_CK(cudaGetLastError());
@@ -2270,7 +2326,7 @@ void trace_run(const TraceArgs& A, TraceResult* R, cudaStream_t s) {
       double* Dt;
       BB_CK(pool.alloc((void**)&Dt, (size_t)nb * 8 + 8));
       {
-        LArgs L{dR, dS, nb, split, Dt, busy_part, aggA, aggC, incA, incC, lflag, ws.counters + 1,
+        LArgs L{dR, dS, nbp, split, Dt, busy_part, aggA, aggC, incA, incC, lflag, ws.counters + 1,
                 tol_rel};
         if (nb) lindley_scan_kernel<<<lt, LB, 0, s>>>(L);
         note_launch();
@@ -2286,7 +2342,7 @@ void trace_run(const TraceArgs& A, TraceResult* R, cudaStream_t s) {
         Bq.S = dS;
         Bq.Dt = Dt;
         Bq.code = split;
-        Bq.nb = nb;
+        Bq.nbp = nbp;
         Bq.tol_rel = tol_rel;
         BB_CK(pool.alloc((void**)&Bq.p0, (size_t)nb * 8));
         BB_CK(pool.alloc((void**)&Bq.p1, (size_t)nb * 8));
@@ -2307,28 +2363,29 @@ void trace_run(const TraceArgs& A, TraceResult* R, cudaStream_t s) {
         note_launch();
         BB_CK(cudaGetLastError());
         binade_chain_kernel<<<grid_for(nb, 128), 128, 0, s>>>(dR, dS, Dt, split, Bq.p0, Bq.p1,
-                                                              Bq.run_last, nb, start, finish, bad);
+                                                              Bq.run_last, nbp, start, finish, bad);
         note_launch();
         BB_CK(cudaGetLastError());
         binade_fill_kernel<<<grid_for(nb, 256), 256, 0, s>>>(dS, Dt, split, Bq.p0, Bq.p1, Bq.head_of,
-                                                             nb, tol_rel, start, finish, bad);
+                                                             nbp, tol_rel, start, finish, bad);
         note_launch();
         BB_CK(cudaGetLastError());
-        lindley_segments_kernel<<<grid_for(nb, 128), 128, 0, s>>>(dR, dS, split, nb, start, finish, bad);
+        lindley_segments_kernel<<<grid_for(nb, 128), 128, 0, s>>>(dR, dS, split, nbp, start, finish, bad);
         note_launch();
         BB_CK(cudaGetLastError());
       }
-      sum_kernel<<<1, 256, 0, s>>>(busy_part, nb ? lt : 0, busy_sum);
+      sum_kernel<<<1, 256, 0, s>>>(busy_part, 0, busy_sum, nbp);
       note_launch();
       BB_CK(cudaGetLastError());
     }
     // per-request pass
     unsigned long long *keys, *kminmax;
     double *lat_part, *lat_sum;
-    const uint32_t qb = grid_for(n, 256);
+    const uint32_t qb = grid_for(n, RQ_T * RQ_E);
+    const uint32_t qb_tm = grid_for(n, 256);
     BB_CK(pool.alloc((void**)&keys, (size_t)n * 8));
     BB_CK(pool.alloc((void**)&kminmax, 16));
-    BB_CK(pool.alloc((void**)&lat_part, (size_t)qb * 8));
+    BB_CK(pool.alloc((void**)&lat_part, (size_t)std::max(qb, qb_tm) * 8));
     BB_CK(pool.alloc((void**)&lat_sum, 8));
     {
       const unsigned long long init[2] = {KEY_UNSERVED, 0ull};
@@ -2351,88 +2408,106 @@ void trace_run(const TraceArgs& A, TraceResult* R, cudaStream_t s) {
       Q.batch = A.req_batch;
       Q.members = A.members;
       if (tm)
-        tm_request_kernel<<<qb, 256, 0, s>>>(A.a, ws.pb8, ws.rank, tm_off, tm_segj, tm_recP, map, finish,
+        tm_request_kernel<<<qb_tm, 256, 0, s>>>(A.a, ws.pb8, ws.rank, tm_off, tm_segj, tm_recP, map, finish,
                                              dfirst, n, keys, lat_part, kminmax, A.req_completion,
                                              A.req_batch, A.members);
       else
-        request_kernel<<<qb, 256, 0, s>>>(Q);
+        request_kernel<<<qb, RQ_T, 0, s>>>(Q);
       note_launch();
       BB_CK(cudaGetLastError());
-      sum_kernel<<<1, 256, 0, s>>>(lat_part, qb, lat_sum);
+      sum_kernel<<<1, 256, 0, s>>>(lat_part, tm ? qb_tm : qb, lat_sum);
       note_launch();
       BB_CK(cudaGetLastError());
     }
+    // exact p50/p99: device-side selection of interpolated_quantile's ranks
+    // (binning.hpp:98-104), computed on the device from the completed count
+    SelState hs{};
+    SelState* ds;
+    {
+      uint32_t* dh;
+      unsigned long long* dc;
+      const uint32_t cap = n < (1u << 22) ? n : (1u << 22);
+      BB_CK(pool.alloc((void**)&ds, sizeof(SelState)));
+      BB_CK(pool.alloc((void**)&dh, HBINS * 4));
+      BB_CK(pool.alloc((void**)&dc, (size_t)cap * 8));
+      BB_CK(cudaMemsetAsync(ds, 0, sizeof(SelState), s));
+      BB_CK(cudaMemsetAsync(dh, 0, HBINS * 4, s));
+      int dev = 0, sms = 148;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      sel_init_kernel<<<1, 1, 0, s>>>(ds, kminmax, ws.info);
+      sel_hist_kernel<<<sms * 4, 256, 0, s>>>(keys, n, ds, dh);
+      sel_find_kernel<<<1, 1024, 0, s>>>(ds, dh, 0xFFFFFFFFu);
+      uint32_t* dh2;
+      BB_CK(pool.alloc((void**)&dh2, (size_t)kSelMax * kSub * 4));
+      BB_CK(cudaMemsetAsync(dh2, 0, (size_t)kSelMax * kSub * 4, s));
+      sel_hist2_kernel<<<sms * 2, 512, 0, s>>>(keys, n, ds, dh2);
+      sel_find2_kernel<<<1, 1024, 0, s>>>(ds, dh2, cap);
+      sel_collect_kernel<<<sms * 4, 256, 0, s>>>(keys, n, ds, dc, cap);
+      sel_refine_kernel<<<1, 1024, 0, s>>>(ds, dc);
+      note_launch(7);
+      BB_CK(cudaGetLastError());
+    }
+    double* scal;  // last completion, first arrival
+    BB_CK(pool.alloc((void**)&scal, 16));
+    scalars_kernel<<<1, 1, 0, s>>>(ws.info, finish, A.n_servers > 1 ? last_dev : nullptr, A.a, scal);
+    note_launch();
     BB_CK(cudaEventRecord(ev2, s));
-    // detail copies of the dispatch-ordered batch records
-    if (A.bat_formed) BB_CK(cudaMemcpyAsync(A.bat_formed, dR, (size_t)nb * 8, cudaMemcpyDeviceToDevice, s));
-    if (A.bat_service) BB_CK(cudaMemcpyAsync(A.bat_service, dS, (size_t)nb * 8, cudaMemcpyDeviceToDevice, s));
-    if (A.bat_first) BB_CK(cudaMemcpyAsync(A.bat_first, dfirst, (size_t)nb * 4, cudaMemcpyDeviceToDevice, s));
-    double last = 0, a0 = 0, busy = 0, lsum = 0;
+    // one host round trip for everything the host reports
+    double sc[2] = {0, 0}, busy = 0, lsum = 0;
     unsigned long long mm[2];
-    if (A.n_servers > 1) BB_CK(cudaMemcpyAsync(&last, last_dev, 8, cudaMemcpyDeviceToHost, s));
-    else if (nb) BB_CK(cudaMemcpyAsync(&last, finish + nb - 1, 8, cudaMemcpyDeviceToHost, s));
-    BB_CK(cudaMemcpyAsync(&a0, A.a, 8, cudaMemcpyDeviceToHost, s));
+    if (!host_sync) {
+      BB_CK(cudaMemcpyAsync(&info, ws.info, sizeof(Info), cudaMemcpyDeviceToHost, s));
+      BB_CK(cudaMemcpyAsync(&herr, ws.err, sizeof(DevError), cudaMemcpyDeviceToHost, s));
+    }
+    BB_CK(cudaMemcpyAsync(sc, scal, 16, cudaMemcpyDeviceToHost, s));
     BB_CK(cudaMemcpyAsync(&busy, busy_sum, 8, cudaMemcpyDeviceToHost, s));
     BB_CK(cudaMemcpyAsync(&lsum, lat_sum, 8, cudaMemcpyDeviceToHost, s));
     BB_CK(cudaMemcpyAsync(mm, kminmax, 16, cudaMemcpyDeviceToHost, s));
+    BB_CK(cudaMemcpyAsync(&hs, ds, sizeof hs, cudaMemcpyDeviceToHost, s));
     BB_CK(cudaStreamSynchronize(s));
+    if (!host_sync) {
+      if (input_error()) goto cleanup;
+      R->path = (int32_t)info.path;
+    }
+    if (!tm) {  // (the timer path counted its own batches)
+      nb = info.nb;
+      nc_run = info.nc;
+      for (uint32_t b = 0; b < k; ++b) R->per_bin[b] = info.nbat[b];
+    }
+    R->n_batches = nb;
+    R->n_completed = nc_run;
+    // detail copies of the dispatch-ordered batch records
+    if (A.bat_formed || A.bat_service || A.bat_first) {
+      if (A.bat_formed) BB_CK(cudaMemcpyAsync(A.bat_formed, dR, (size_t)nb * 8, cudaMemcpyDeviceToDevice, s));
+      if (A.bat_service) BB_CK(cudaMemcpyAsync(A.bat_service, dS, (size_t)nb * 8, cudaMemcpyDeviceToDevice, s));
+      if (A.bat_first) BB_CK(cudaMemcpyAsync(A.bat_first, dfirst, (size_t)nb * 4, cudaMemcpyDeviceToDevice, s));
+      BB_CK(cudaStreamSynchronize(s));
+    }
     const unsigned long long nc = nc_run;
     if (nc > 0) {  // finish(), simulator.hpp:283-301
+      const double last = sc[0], a0 = sc[1];
       R->makespan = last - a0;
       R->throughput = (double)nc / R->makespan;
       R->busy = busy;
       R->busy_fraction = busy / ((double)(A.n_servers > 1 ? A.n_servers : 1) * R->makespan);
       R->latency_sum = lsum;
       R->latency_mean = lsum / (double)nc;
-      // interpolated_quantile, binning.hpp:98-104
+      // interpolated_quantile, binning.hpp:98-104 (the ranks sel_init_kernel selected)
       const double qs[2] = {0.50, 0.99};
-      std::vector<unsigned long long> ranks;
+      std::vector<unsigned long long> ranks(hs.rank, hs.rank + hs.nt);
       unsigned long long idxs[2];
       double fracs[2];
       for (int q = 0; q < 2; ++q) {
         const volatile double pos = qs[q] * (double)(nc - 1);
         idxs[q] = (unsigned long long)pos;
         fracs[q] = pos - (double)idxs[q];
-        ranks.push_back(idxs[q]);
-        if (idxs[q] + 1 < nc) ranks.push_back(idxs[q] + 1);
       }
       std::vector<unsigned long long> vals;
-      {
-        // device-side selection (single sync); multi-launch refine as the fallback
-        SelState hs{};
-        hs.nt = (uint32_t)ranks.size();
-        for (size_t q = 0; q < ranks.size(); ++q) hs.rank[q] = ranks[q];
-        SelState* ds;
-        uint32_t* dh;
-        unsigned long long* dc;
-        const uint32_t cap = n < (1u << 22) ? n : (1u << 22);
-        BB_CK(pool.alloc((void**)&ds, sizeof(SelState)));
-        BB_CK(pool.alloc((void**)&dh, HBINS * 4));
-        BB_CK(pool.alloc((void**)&dc, (size_t)cap * 8));
-        BB_CK(cudaMemcpyAsync(ds, &hs, sizeof hs, cudaMemcpyHostToDevice, s));
-        BB_CK(cudaMemsetAsync(dh, 0, HBINS * 4, s));
-        int dev = 0, sms = 148;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        sel_init_kernel<<<1, 1, 0, s>>>(ds, kminmax);
-        sel_hist_kernel<<<sms * 4, 256, 0, s>>>(keys, n, ds, dh);
-        sel_find_kernel<<<1, 1024, 0, s>>>(ds, dh, 0xFFFFFFFFu);
-        uint32_t* dh2;
-        BB_CK(pool.alloc((void**)&dh2, (size_t)kSelMax * kSub * 4));
-        BB_CK(cudaMemsetAsync(dh2, 0, (size_t)kSelMax * kSub * 4, s));
-        sel_hist2_kernel<<<sms * 2, 512, 0, s>>>(keys, n, ds, dh2);
-        sel_find2_kernel<<<1, 1024, 0, s>>>(ds, dh2, cap);
-        sel_collect_kernel<<<sms * 4, 256, 0, s>>>(keys, n, ds, dc, cap);
-        sel_refine_kernel<<<1, 1024, 0, s>>>(ds, dc);
-        note_launch(7);
-        BB_CK(cudaGetLastError());
-        BB_CK(cudaMemcpyAsync(&hs, ds, sizeof hs, cudaMemcpyDeviceToHost, s));
-        BB_CK(cudaStreamSynchronize(s));
-        if (hs.overflow) {
-          BB_CK(select_ranks(keys, n, mm[0], mm[1], ranks, vals, pool, s));
-        } else {
-          for (size_t q = 0; q < ranks.size(); ++q) vals.push_back(hs.result[q]);
-        }
+      if (hs.overflow) {  // multi-launch refine as the fallback
+        BB_CK(select_ranks(keys, n, mm[0], mm[1], ranks, vals, pool, s));
+      } else {
+        for (size_t q = 0; q < ranks.size(); ++q) vals.push_back(hs.result[q]);
       }
       size_t vi = 0;
       double outq[2];
