@@ -220,35 +220,50 @@ struct QFast {
       }
       if (valid) k_p[off] = (uint16_t)b;
     };
-    // software pipeline: the next chunk's arrivals and ids are in flight
-    // while this chunk's completions are gathered and used
-    constexpr int C = kQChunk;
+    // three-stage software pipeline over chunks of C runs: while chunk t is
+    // used, chunk t+1's completions (gathered by its batch ids) and chunk
+    // t+2's arrivals and ids are in flight -- the id -> completion gather
+    // is a second dependent round trip, so it is issued one chunk early
+#ifndef BB_QL0C
+#define BB_QL0C 6
+#endif
+    constexpr int C = BB_QL0C;
+    constexpr uint32_t R = 32 * kQRun;
     uint32_t t = 0;
-    double na[C];
-    uint32_t nid[C];
-    if (C <= full) {
+    double a1[C], f1[C], a2[C];
+    uint32_t i2[C];
+    if (2 * C <= full) {
 #pragma unroll
       for (int u = 0; u < C; ++u) {
-        na[u] = a_p[u * (32 * kQRun)];
-        nid[u] = i_p[u * (32 * kQRun)];
+        a1[u] = a_p[u * R];
+        a2[u] = a_p[(C + u) * R];
+        i2[u] = i_p[(C + u) * R];
       }
-    }
-    for (; t + C <= full; t += C) {
-      double a[C], f[C];
 #pragma unroll
-      for (int u = 0; u < C; ++u) {
-        a[u] = na[u];
-        f[u] = F[nid[u]];
-      }
-      if (t + 2 * C <= full) {
+      for (int u = 0; u < C; ++u) f1[u] = F[i_p[u * R]];
+      for (; t + 2 * C <= full; t += C) {
+        double a[C], f[C];
 #pragma unroll
         for (int u = 0; u < C; ++u) {
-          na[u] = a_p[(t + C + u) * (32 * kQRun)];
-          nid[u] = i_p[(t + C + u) * (32 * kQRun)];
+          a[u] = a1[u];
+          f[u] = f1[u];
+          a1[u] = a2[u];
+          f1[u] = F[i2[u]];  // chunk t+1
         }
-      }
+        if (t + 3 * C <= full) {
 #pragma unroll
-      for (int u = 0; u < C; ++u) one(a[u], f[u], true, (t + u) * (32 * kQRun));
+          for (int u = 0; u < C; ++u) {  // chunk t+2
+            a2[u] = a_p[(t + 2 * C + u) * R];
+            i2[u] = i_p[(t + 2 * C + u) * R];
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < C; ++u) one(a[u], f[u], true, (t + u) * R);
+      }
+      // chunk t (its a1/f1 are loaded) is the last full one of the pipeline
+#pragma unroll
+      for (int u = 0; u < C; ++u) one(a1[u], f1[u], true, (t + u) * R);
+      t += C;
     }
     for (; t < nt; ++t) {
       const bool v = t * 32 + lane < n;
