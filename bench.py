@@ -577,7 +577,7 @@ def trace_measure(bb, torch, dev, stream, n=10_000_000):
             "e2e": {"value": n / te, "unit": "requests/s", "ms_per_run": te * 1e3,
                     "h2d_bytes_per_step": int(n * 17), "d2h_bytes_per_step": __import__("ctypes").sizeof(bb._capi.SimMetricsC),
                     "api": "bb_run_trace (pinned host arrays in, host metrics out)"},
-            "roofline": {"bound": "hbm", "kernel": "partition_kernel", "kernel_ms": tp,
+            "roofline": {"bound": "hbm", "kernel": "partition (count_kernel + tscan_kernel + place_kernel)", "kernel_ms": tp,
                          "achieved": part_bytes / (tp / 1e3) / 1e9,
                          "peak": measured_peaks()["hbm_gbs"], "unit": "GB/s",
                          "frac": part_bytes / (tp / 1e3) / 1e9 / measured_peaks()["hbm_gbs"],

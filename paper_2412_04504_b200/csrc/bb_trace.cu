@@ -86,6 +86,7 @@ struct PartArgs {
   const double* conf;
   uint8_t* tb_out;
   uint32_t n, B, k, ntiles;
+  uint32_t vec_ok;  // every array 16-byte aligned (8 for the predictions): vector and bulk loads
   int32_t err_kind;
   double p, one_minus_p;
   FastDiv divB;
@@ -122,6 +123,7 @@ __device__ __forceinline__ uint32_t assign_bin(const double* e, uint32_t k, doub
 //                 sum_b floor(prefix_b / B))
 constexpr int PT = 256, PIPT = 8, PTILE = PT * PIPT, PNW = PT / 32;
 
+
 // the predicted bin of request idx (0: invalid, error raised); tb: true bin
 __device__ __forceinline__ uint32_t part_bin(const PartArgs& P, const double* edges, uint64_t idx,
                                              double sv, uint32_t& tb) {
@@ -156,36 +158,97 @@ __device__ __forceinline__ uint32_t part_bin(const PartArgs& P, const double* ed
   return tb;
 }
 
+// Counting needs no order: thread t takes the PIPT consecutive requests at
+// tile + t * PIPT, loaded as one 8-byte vector of predictions (or 16-byte
+// vectors of services and error uniforms) when aligned.
 __global__ void __launch_bounds__(PT) count_kernel(PartArgs P) {
   __shared__ double s_edges[BB_TRACE_MAX_BINS + 1];
   __shared__ uint32_t s_cnt[PNW][32];
+  static_assert(PIPT == 8, "one 8-byte vector of predictions per thread");
   const uint32_t tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const uint32_t k = P.k, n = P.n;
   for (uint32_t i = tid; i <= k; i += PT) s_edges[i] = P.edges[i];
-  s_cnt[w][lane] = 0;
   __syncthreads();
-  const uint64_t base = (uint64_t)blockIdx.x * PTILE + w * (32 * PIPT);
-#pragma unroll 4
-  for (int j = 0; j < PIPT; ++j) {
-    const uint64_t idx = base + j * 32 + lane;
-    uint32_t b = 0;
-    if (idx < n) {
-      if (P.pred) {
-        b = P.pred[idx];
-        if (b < 1 || b > k) {
-          raise_error(P.ws.err, idx, BB_EINVAL, (double)b, 3);
-          b = 0;
-        }
-      } else {
-        uint32_t tb;
-        b = part_bin(P, s_edges, idx, P.s[idx], tb);
-        P.ws.pb8[idx] = (uint8_t)b;
-        if (P.tb_out) P.tb_out[idx] = (uint8_t)tb;
-      }
+  const uint64_t i0 = (uint64_t)blockIdx.x * PTILE + (uint64_t)tid * PIPT;
+  const bool full = i0 + PIPT <= n && P.vec_ok;
+  uint32_t b[PIPT];
+  if (P.pred) {
+    if (full) {
+      const uint2 v = *reinterpret_cast<const uint2*>(P.pred + i0);
+#pragma unroll
+      for (int j = 0; j < PIPT; ++j) b[j] = ((j < 4 ? v.x : v.y) >> (8 * (j & 3))) & 0xFF;
+    } else {
+#pragma unroll
+      for (int j = 0; j < PIPT; ++j) b[j] = i0 + j < n ? P.pred[i0 + j] : 0u;
     }
-    const uint32_t peers = __match_any_sync(0xffffffffu, b);  // the bin's lowest lane adds them
-    if (b && !(peers & lanemask_lt())) s_cnt[w][b - 1] += __popc(peers);
-    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < PIPT; ++j)
+      if (i0 + j < n && (b[j] < 1 || b[j] > k)) {
+        raise_error(P.ws.err, i0 + j, BB_EINVAL, (double)b[j], 3);
+        b[j] = 0;
+      }
+  } else {
+    double sv[PIPT];
+    if (full) {
+#pragma unroll
+      for (int j = 0; j < PIPT; j += 2) {
+        const double2 x = *reinterpret_cast<const double2*>(P.s + i0 + j);
+        sv[j] = x.x;
+        sv[j + 1] = x.y;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < PIPT; ++j) sv[j] = i0 + j < n ? P.s[i0 + j] : 0.0;
+    }
+    uint32_t tbs[PIPT];
+#pragma unroll
+    for (int j = 0; j < PIPT; ++j) {
+      b[j] = tbs[j] = 0;
+      if (i0 + j < n) b[j] = part_bin(P, s_edges, i0 + j, sv[j], tbs[j]);
+    }
+    if (full) {  // predicted (and true) bins, one vector store each
+      uint2 pv = make_uint2(0, 0), tv = make_uint2(0, 0);
+#pragma unroll
+      for (int j = 0; j < PIPT; ++j) {
+        (j < 4 ? pv.x : pv.y) |= b[j] << (8 * (j & 3));
+        (j < 4 ? tv.x : tv.y) |= tbs[j] << (8 * (j & 3));
+      }
+      *reinterpret_cast<uint2*>(P.ws.pb8 + i0) = pv;
+      if (P.tb_out) *reinterpret_cast<uint2*>(P.tb_out + i0) = tv;
+    } else {
+#pragma unroll
+      for (int j = 0; j < PIPT; ++j)
+        if (i0 + j < n) {
+          P.ws.pb8[i0 + j] = (uint8_t)b[j];
+          if (P.tb_out) P.tb_out[i0 + j] = (uint8_t)tbs[j];
+        }
+    }
+  }
+  // per-thread counts in 4-bit fields (bin q+1 at nib[q / 8], bits 4 (q % 8);
+  // at most PIPT = 8 per thread), then spread to 16-bit fields and summed over
+  // the warp with one integer reduction per four bins (<= 256 per field)
+  uint32_t nib[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+  for (int j = 0; j < PIPT; ++j) {
+    const uint32_t q = b[j] - 1, inc = b[j] ? 1u << (4 * (q & 7)) : 0u;
+#pragma unroll
+    for (int g = 0; g < 4; ++g) nib[g] += (q >> 3) == (uint32_t)g ? inc : 0u;
+  }
+  const uint32_t ng = (k + 7) / 8;
+#pragma unroll
+  for (int g = 0; g < 4; ++g) {
+    if ((uint32_t)g >= ng) break;
+    const uint32_t ev = nib[g] & 0x0F0F0F0Fu, od = (nib[g] >> 4) & 0x0F0F0F0Fu;
+    const uint32_t r0 = __reduce_add_sync(0xffffffffu, ev & 0x00FF00FFu);         // bins 8g+1, +5
+    const uint32_t r1 = __reduce_add_sync(0xffffffffu, (ev >> 8) & 0x00FF00FFu);  // bins 8g+3, +7
+    const uint32_t r2 = __reduce_add_sync(0xffffffffu, od & 0x00FF00FFu);         // bins 8g+2, +6
+    const uint32_t r3 = __reduce_add_sync(0xffffffffu, (od >> 8) & 0x00FF00FFu);  // bins 8g+4, +8
+    if (lane == 0) {
+      const uint32_t c[8] = {r0 & 0xFFFF, r2 & 0xFFFF, r1 & 0xFFFF, r3 & 0xFFFF,
+                             r0 >> 16, r2 >> 16, r1 >> 16, r3 >> 16};
+#pragma unroll
+      for (int q = 0; q < 8; ++q) s_cnt[w][8 * g + q] = c[q];
+    }
   }
   __syncthreads();
   if (w == 0 && lane < k) {
@@ -311,14 +374,18 @@ __global__ void __launch_bounds__(PT, 3) place_kernel(PartArgs P) {
     av[j] = v ? P.a[idx] : 0.0;
     sv[j] = v ? P.s[idx] : 0.0;
     pr[j] = v ? pbsrc[idx] : 0u;
+    if (pr[j] > k) pr[j] = 0;  // an invalid given prediction (count_kernel reported it)
   }
-  uint32_t flags = 0;
+  uint32_t flags = 0, ties = 0;
   const uint32_t lt = lanemask_lt();
+  const double e_lo = s_edges[0], e_hi = s_edges[k];
+  uint32_t pbk[PIPT / 4] = {};  // the bins, packed (the records need them after pr holds ranks)
 #pragma unroll
   for (int j = 0; j < PIPT; ++j) {
     const uint64_t idx = wbase + j * 32 + lane;
     const bool valid = idx < n;
     const uint32_t pb = pr[j];
+    pbk[j / 4] |= pb << (8 * (j & 3));
     // predecessor arrival for the monotonicity / tie checks
     double prev = __shfl_up_sync(0xffffffffu, av[j], 1);
     const double prevj = __shfl_sync(0xffffffffu, av[j > 0 ? j - 1 : 0], 31);
@@ -326,16 +393,19 @@ __global__ void __launch_bounds__(PT, 3) place_kernel(PartArgs P) {
     if (valid) {
       if (idx > 0) {
         if (!(av[j] >= prev)) flags |= FL_NONMONO;
-        else if (av[j] == prev && idx >= B && P.a[idx - B] == av[j]) flags |= FL_TIE_GT_B;
+        else if (av[j] == prev) ties |= 1u << j;  // checked against a[idx - B] below (rare)
       }
       if (av[j] != a0) flags |= FL_NOT_ALL_EQUAL;
       if (P.pred) {  // given predictions: the services are still checked (and binned)
-        uint32_t tb = 0;
-        const double s = sv[j];
-        if (!(s > 0) || !isfinite(s)) raise_error(P.ws.err, idx, BB_EDOMAIN, s, 1);
-        else if (TBOUT ? (tb = assign_bin(s_edges, k, s)) == 0 : !(s >= s_edges[0] && s <= s_edges[k]))
-          raise_error(P.ws.err, idx, BB_EDOMAIN, s, 2);
-        if (TBOUT) P.tb_out[idx] = (uint8_t)tb;
+        const double sj = sv[j];
+        if (TBOUT) {
+          uint32_t tb = 0;
+          if (!(sj > 0) || !isfinite(sj)) raise_error(P.ws.err, idx, BB_EDOMAIN, sj, 1);
+          else if ((tb = assign_bin(s_edges, k, sj)) == 0) raise_error(P.ws.err, idx, BB_EDOMAIN, sj, 2);
+          P.tb_out[idx] = (uint8_t)tb;
+        } else if (!(sj > 0 && sj < CUDART_INF && sj >= e_lo && sj <= e_hi)) {
+          raise_error(P.ws.err, idx, BB_EDOMAIN, sj, !(sj > 0) || !isfinite(sj) ? 1 : 2);
+        }
       }
     }
     // stable rank within the warp's requests of the same bin (match_any)
@@ -346,6 +416,13 @@ __global__ void __launch_bounds__(PT, 3) place_kernel(PartArgs P) {
     __syncwarp();
     if (pb && !(mine & lt)) s_run[w][pb - 1] = run + __popc(mine);
     __syncwarp();
+  }
+  if (ties) {  // a run of equal arrivals: longer than B?
+#pragma unroll
+    for (int j = 0; j < PIPT; ++j) {
+      const uint64_t idx = wbase + j * 32 + lane;
+      if (((ties >> j) & 1u) && idx >= B && P.a[idx - B] == av[j]) flags |= FL_TIE_GT_B;
+    }
   }
   if (flags) atomicOr(&s_flags, flags);
   __syncthreads();
@@ -409,7 +486,7 @@ __global__ void __launch_bounds__(PT, 3) place_kernel(PartArgs P) {
       const uint64_t idx = wbase + j * 32 + lane;
       const uint32_t q = run + __popc(bal & lt);
       P.ws.recR[q] = av[j];
-      P.ws.recBin[q] = pbsrc[idx];
+      P.ws.recBin[q] = (uint8_t)(pbk[j / 4] >> (8 * (j & 3)));
       P.ws.recJ[q] = P.divB.div(pr[j]);
       P.ws.recC[q] = (uint32_t)idx;
     }
@@ -615,7 +692,10 @@ __global__ void __launch_bounds__(256) tie_order_kernel(TieArgs T) {
       const uint32_t t = x / PTILE;
       if (tid < k)
         atomicAdd(&s_c[side][tid], t < T.ntiles ? T.ws.tcount[(uint64_t)tid * T.ntiles + t] : (uint32_t)T.ws.fin_cnt[tid]);
-      for (uint32_t i = t * PTILE + tid; i < x; i += blockDim.x) atomicAdd(&s_c[side][T.ws.pb8[i] - 1], 1u);
+      for (uint32_t i = t * PTILE + tid; i < x; i += blockDim.x) {
+        const uint32_t b = T.ws.pb8[i];
+        if (b - 1u < k) atomicAdd(&s_c[side][b - 1], 1u);
+      }
     }
     __syncthreads();
     if (tid < 32) {
@@ -948,6 +1028,17 @@ __device__ __forceinline__ PMap batch_map(double S, int e) {
   return PMap{q + up + (half & (q & 1)), q + up + (half & ((q + 1) & 1))};
 }
 
+// What the chain walk needs of a run, written once at its last batch: one
+// dependent load per run head instead of three.
+struct RunInfo {
+  long long p0, p1;   // prefix map of the run's last batch
+  double Rn, Sn;      // formation time and service of the batch after the run
+  uint32_t last;      // the run's last batch
+  int32_t e;          // the binade predicted for the run's last value
+  uint32_t next_code; // split code of the batch after the run (kSplit: the busy period ends)
+  uint32_t pad;
+};
+
 struct BArgs {
   const double* R;
   const double* S;
@@ -959,6 +1050,7 @@ struct BArgs {
   long long* p1;
   uint32_t* head_of;   // run head of each batch
   uint32_t* run_last;  // last batch of each run, indexed by head
+  RunInfo* run_info;   // ... and what the chain walk needs of it, indexed by head
   // look-back
   long long *ag0, *ag1, *in0, *in1;
   uint32_t *agh, *inh, *agf, *inf;  // head position (+1, 0 = none) and head flag
@@ -1094,30 +1186,29 @@ __global__ void __launch_bounds__(LB) binade_scan_kernel(BArgs A) {
     A.head_of[d] = h;
     bool last = d + 1 == nb;
     if (!last) last = run_head(A.code[d + 1], A.Dt[d], A.Dt[d + 1], A.tol_rel);
-    if (last) A.run_last[h] = (uint32_t)d;
+    if (last) {
+      A.run_last[h] = (uint32_t)d;
+      RunInfo ri;
+      ri.p0 = r.m.i0;
+      ri.p1 = r.m.i1;
+      ri.last = (uint32_t)d;
+      ri.e = binade(A.Dt[d]);
+      const bool more = d + 1 < nb;
+      ri.next_code = more ? A.code[d + 1] : (uint32_t)kSplit;
+      ri.Rn = more ? A.R[d + 1] : 0.0;
+      ri.Sn = more ? A.S[d + 1] : 0.0;
+      ri.pad = 0;
+      A.run_info[h] = ri;
+    }
   }
 }
 
-// value of the run's last batch from its head value (exact), or a fallback flag
-__device__ __forceinline__ double run_end(double Dh, uint32_t h, uint32_t last, const double* Dt,
-                                          const long long* p0, const long long* p1, int* bad) {
-  if (last == h) return Dh;
-  const int e = binade(Dt[last]);
-  if (binade(Dh) != e) {
-    *bad = 1;
-    return Dh;
-  }
-  const long long a = (long long)ldexp(Dh, 52 - e);
-  const long long al = a + ((a & 1) ? p1[last] : p0[last]);
-  if (al > (1ll << 53)) *bad = 1;
-  return ldexp((double)al, e - 52);
-}
 
 // one thread per busy period: walk its run heads (exact fp64 steps)
 __global__ void binade_chain_kernel(const double* __restrict__ R, const double* __restrict__ S,
                                     const double* __restrict__ Dt, const uint8_t* __restrict__ code,
                                     const long long* __restrict__ p0, const long long* __restrict__ p1,
-                                    const uint32_t* __restrict__ run_last, const uint32_t* nbp,
+                                    const RunInfo* __restrict__ run_info, const uint32_t* nbp,
                                     double* __restrict__ start, double* __restrict__ finish,
                                     int* bad) {
   const uint32_t nb = *nbp;
@@ -1128,13 +1219,22 @@ __global__ void binade_chain_kernel(const double* __restrict__ R, const double* 
   start[h] = R[h];
   finish[h] = D;
   while (true) {
-    const uint32_t last = run_last[h];
-    D = run_end(D, h, last, Dt, p0, p1, bad);
-    const uint32_t nx = last + 1;
-    if (nx >= nb || code[nx] == kSplit) return;
+    const RunInfo ri = run_info[h];  // the walk's only dependent load per run
+    if (ri.last != h) {  // run_end: the head's value through the run's prefix map
+      if (binade(D) != ri.e) {
+        *bad = 1;
+        return;
+      }
+      const long long a = (long long)ldexp(D, 52 - ri.e);
+      const long long al = a + ((a & 1) ? ri.p1 : ri.p0);
+      if (al > (1ll << 53)) *bad = 1;
+      D = ldexp((double)al, ri.e - 52);
+    }
+    const uint32_t nx = ri.last + 1;
+    if (nx >= nb || ri.next_code == kSplit) return;
     h = nx;
-    const double st = fmax(D, R[h]);  // ambiguous reset or binade crossing: exact step
-    D = __dadd_rn(st, S[h]);
+    const double st = fmax(D, ri.Rn);  // ambiguous reset or binade crossing: exact step
+    D = __dadd_rn(st, ri.Sn);
     start[h] = st;
     finish[h] = D;
   }
@@ -1177,7 +1277,7 @@ struct QArgs {
   const uint32_t* dfirst;
   const Info* info;
   FastDiv divB;
-  uint32_t n, B;
+  uint32_t n, B, k;
   unsigned long long* key;
   double* lat_part;
   unsigned long long* kminmax;
@@ -1271,6 +1371,7 @@ __global__ void __launch_bounds__(RQ_T) request_kernel(QArgs Q) {
     const uint64_t i = base + e * RQ_T;
     const bool v = i < Q.n;
     bin[e] = v ? Q.pb8[i] : 0u;
+    if (bin[e] > Q.k) bin[e] = 0;  // an invalid given prediction: the run reports the error
     rk[e] = v ? Q.rank[i] : 0u;
     a[e] = v ? Q.a[i] : 0.0;
   }
@@ -1880,16 +1981,52 @@ __global__ void __launch_bounds__(256) tm_request_kernel(
     }                                                                                   \
   } while (0)
 
+// Scratch of one trace run: a bump allocator over a per-device arena of
+// cached chunks (no allocation API call per buffer; the pipeline asks for
+// ~50 buffers).  Callers hold the device's mutex, so one run uses the arena
+// at a time; a run's stream waits for the previous run's end event before
+// reusing the memory (runs may come on different streams).
+struct Arena {
+  std::vector<std::pair<char*, size_t>> chunks;
+  cudaEvent_t done = nullptr;
+};
+Arena g_arena[64];
+
 struct Pool {
-  std::vector<void*> ptrs;
-  cudaStream_t s;
+  cudaStream_t s = nullptr;
+  Arena* ar = nullptr;
+  size_t chunk = 0, off = 0;
   cudaError_t alloc(void** p, size_t bytes) {
-    cudaError_t e = cudaMallocAsync(p, bytes ? bytes : 8, s);
-    if (e == cudaSuccess) ptrs.push_back(*p);
-    return e;
+    if (!ar) {  // first use in this run
+      int dev = 0;
+      cudaGetDevice(&dev);
+      ar = &g_arena[dev & 63];
+      if (ar->done) {
+        cudaError_t e = cudaStreamWaitEvent(s, ar->done, 0);
+        if (e != cudaSuccess) return e;
+      }
+    }
+    bytes = ((bytes ? bytes : 8) + 255) & ~(size_t)255;
+    while (chunk < ar->chunks.size() && off + bytes > ar->chunks[chunk].second) {
+      ++chunk;
+      off = 0;
+    }
+    if (chunk == ar->chunks.size()) {
+      const size_t cb = bytes > ((size_t)256 << 20) ? bytes : ((size_t)256 << 20);
+      char* c = nullptr;
+      cudaError_t e = cudaMalloc(&c, cb);
+      if (e != cudaSuccess) return e;
+      ar->chunks.push_back({c, cb});
+      off = 0;
+    }
+    *p = ar->chunks[chunk].first + off;
+    off += bytes;
+    return cudaSuccess;
   }
   ~Pool() {
-    for (void* p : ptrs) cudaFreeAsync(p, s);
+    if (!ar) return;
+    if (!ar->done) cudaEventCreateWithFlags(&ar->done, cudaEventDisableTiming);
+    cudaEventRecord(ar->done, s);
   }
 };
 
@@ -2055,6 +2192,11 @@ void trace_run(const TraceArgs& A, TraceResult* R, cudaStream_t s) {
     P.one_minus_p = 1.0 - A.p_error;
     P.divB = FastDiv(B);
     P.ws = ws;
+    {
+      auto al = [](const void* q, uintptr_t m) { return ((uintptr_t)q & (m - 1)) == 0; };
+      P.vec_ok = al(A.a, 16) && al(A.s, 16) && (!A.u_err || al(A.u_err, 16)) && (!A.pred || al(A.pred, 16)) &&
+                 al(ws.pb8, 16) && (!A.req_true_bin || al(A.req_true_bin, 16));
+    }
     count_kernel<<<ntiles, PT, 0, s>>>(P);
     tscan_kernel<<<k, TS_T, 0, s>>>(ws, ntiles, k, B);
     sbase_kernel<<<1, 1, 0, s>>>(ws, k, B);
@@ -2348,6 +2490,7 @@ void trace_run(const TraceArgs& A, TraceResult* R, cudaStream_t s) {
         BB_CK(pool.alloc((void**)&Bq.p1, (size_t)nb * 8));
         BB_CK(pool.alloc((void**)&Bq.head_of, (size_t)nb * 4));
         BB_CK(pool.alloc((void**)&Bq.run_last, (size_t)nb * 4));
+        BB_CK(pool.alloc((void**)&Bq.run_info, (size_t)nb * sizeof(RunInfo)));
         BB_CK(pool.alloc((void**)&Bq.ag0, (size_t)lt * 8));
         BB_CK(pool.alloc((void**)&Bq.ag1, (size_t)lt * 8));
         BB_CK(pool.alloc((void**)&Bq.in0, (size_t)lt * 8));
@@ -2363,7 +2506,7 @@ void trace_run(const TraceArgs& A, TraceResult* R, cudaStream_t s) {
         note_launch();
         BB_CK(cudaGetLastError());
         binade_chain_kernel<<<grid_for(nb, 128), 128, 0, s>>>(dR, dS, Dt, split, Bq.p0, Bq.p1,
-                                                              Bq.run_last, nbp, start, finish, bad);
+                                                              Bq.run_info, nbp, start, finish, bad);
         note_launch();
         BB_CK(cudaGetLastError());
         binade_fill_kernel<<<grid_for(nb, 256), 256, 0, s>>>(dS, Dt, split, Bq.p0, Bq.p1, Bq.head_of,
@@ -2401,6 +2544,7 @@ void trace_run(const TraceArgs& A, TraceResult* R, cudaStream_t s) {
       Q.divB = FastDiv(B);
       Q.n = n;
       Q.B = B;
+      Q.k = k;
       Q.key = keys;
       Q.lat_part = lat_part;
       Q.kminmax = kminmax;
