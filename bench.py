@@ -254,7 +254,12 @@ def main():
             dist.init_process_group("nccl", device_id=dev)
         else:  # functional testing of the N>1 path on a single GPU
             dist.init_process_group(args.dist_backend)
-    stream = torch.cuda.current_stream()
+    # one explicit stream for torch's own ops and the engine's launches (the
+    # engine's stream-ordered entries run on the stream they are handed; the
+    # legacy default stream's handle is 0, which the C ABI reads as "the
+    # library's own stream")
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)
     sptr = stream.cuda_stream
 
     pts = sweep_points(args.requests)
@@ -359,9 +364,8 @@ def main():
         qbytes = ALG_BYTES_QUANTILES * requests_step if quant else 0.0
         t_hbm = qbytes / hbm_peak
         traffic = None
-        prof = os.path.join(ROOT, "profiles", "r01_gen_kernel_q_ncu.json" if quant
-                            else "r01_gen_kernel_ncu.json")
-        if os.path.exists(prof):  # one `ncu --set full` capture; scaled per launch
+        prof = latest_profile("gen_kernel_q_ncu.json" if quant else "gen_kernel_ncu.json")
+        if prof:  # one `ncu --set full` capture; scaled per launch
             cap = json.load(open(prof))
             cap = cap[0] if isinstance(cap, list) else cap
             if cap.get("dram_bytes_per_request") is not None:
@@ -484,6 +488,15 @@ def c5_measure(bb, torch, stream, reps=148 * 16 * 32, n=1_000_000):
             "latency_p99_mean": p.latency_p99}
 
 
+def latest_profile(name):
+    """profiles/r<NN>_<name> of the latest round that has it (ncu summaries)."""
+    d = os.path.join(ROOT, "profiles")
+    if not os.path.isdir(d):
+        return None
+    hits = sorted(f for f in os.listdir(d) if f.startswith("r") and f.endswith("_" + name))
+    return os.path.join(d, hits[-1]) if hits else None
+
+
 def trace_measure(bb, torch, dev, stream, n=10_000_000):
     """Secondary: BASELINE config 2 (10^7-request trace, k=8, B=16) in trace
     mode with the arrays resident in HBM -- the HBM-bound pipeline.
@@ -563,13 +576,16 @@ def trace_measure(bb, torch, dev, stream, n=10_000_000):
     # partition kernel algorithmic bytes: read a,s (16) + pred (1); write pb (1) + rank (4)
     # + closing records (8+8+1+4+4 per batch = 25/B)
     part_bytes = n * (16 + 1 + 1 + 4) + (n / 16) * 25
-    traffic = None  # DRAM bytes of one partition launch, from one `ncu --set full` capture
-    prof = os.path.join(ROOT, "profiles", "r01_trace_c2_ncu.json")
-    if os.path.exists(prof):
+    traffic = None  # DRAM bytes of one partition (its kernels), from one `ncu --set full` capture
+    prof = latest_profile("trace_c2_ncu.json")
+    if prof:
         caps = json.load(open(prof))
-        for c in (caps if isinstance(caps, list) else [caps]):
-            if "partition_kernel" in c.get("kernel", "") and c.get("dram_bytes_per_request"):
-                traffic = c["dram_bytes_per_request"] * n
+        parts_b = [c["dram_bytes_per_request"] for c in (caps if isinstance(caps, list) else [caps])
+                   if c.get("dram_bytes_per_request") and any(
+                       x in c.get("kernel", "") for x in ("partition_kernel", "count_kernel", "tscan_kernel",
+                                                           "place_kernel"))]
+        if parts_b:
+            traffic = sum(parts_b) * n
     return {"workload": "C2: 10^7-request trace from the reference generator, k=8, B=16, "
                         "lambda=0.95 cap, Symmetric(0.1) predictions as input",
             "value": n / (t / 1e3), "unit": "requests/s", "ms_per_run": t,

@@ -7,24 +7,21 @@
 // (experiment.hpp:262-263,278-279).  The fused kernel keeps one replication
 // per lane in registers, so the latencies are not materialised during the
 // simulation.  Instead the forward pass logs, per request, its arrival time
-// and a byte (predicted bin | closing flag), and per closed batch its
-// completion time; afterwards the warp selects the order statistics of one
-// replication at a time:
+// and its batch's id (batches get ids when their first member arrives), and
+// per batch id its completion time; afterwards the warp selects the order
+// statistics of one replication at a time:
 //
-//   source (finite rate): the request log read backwards in 32-request
-//     tiles.  A request belongs to the batch closed by the next closing
-//     request of its bin (or to its bin's drained partial), so
-//     __match_any_sync over the bins + a ballot of the closing flags give
-//     each lane the completion of its batch; a per-bin carry crosses tiles.
-//     latency = completion - arrival, exactly the reference's subtraction.
+//   source (finite rate): latency_i = F[id_i] - a_i, the reference's
+//     subtraction, for every request independently (QFast::level0 streams
+//     the log with a three-stage software pipeline; QSrcLog for later passes).
 //   source (overload): the batches' completions weighted by member counts.
 //
-//   select: radix histograms over the IEEE bit patterns of the (positive)
-//     latencies -- 2048 buckets per pass, the first pass spanning
-//     [min, max] from the forward pass, each further pass one bucket of the
-//     previous -- until the buckets holding the wanted ranks fit in shared
-//     memory; one more pass collects them and the ranks are resolved by
-//     counting.  Typically two passes over the log (9 B/request each).
+//   select: level 0 is a 2048-bucket histogram of a monotone 32-bit function
+//     of the latencies' IEEE bits over [min, max] from the forward pass,
+//     leaving each request's bucket id; when the wanted ranks' buckets fit
+//     in shared memory one more pass collects them by bucket id (2 B per
+//     request) and the ranks are resolved by 256-bucket refinements and
+//     counting; otherwise further histogram passes narrow the buckets first.
 //
 // Every value is an exact order statistic of the same multiset the reference
 // sorts, and the interpolation uses the reference's operation order without

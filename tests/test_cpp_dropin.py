@@ -107,3 +107,73 @@ def test_reference_unit_suite_unchanged_on_gpu():
     print(r.stdout[-6000:])
     assert r.returncode == 0, r.stdout[-6000:]
     assert "All tests passed" in r.stdout
+
+
+# ---- the reference's own front end (proj/tools/binbatch_cli.cpp), unchanged,
+# built against the reference headers (binbatch_ref) and the drop-in
+# (binbatch_b200) with tests/cpp/cli11_shim standing in for CLI11
+RUN_JSON = {"lambda": 10.0, "n_requests": 12800, "batch_size": 128, "n_servers": 1,
+            "flush_partial": True, "max_batch_wait": None,
+            "service": {"type": "uniform", "min_time": 1.0, "max_time": 20.0},
+            "bins": {"k": 5}, "error": {"type": "symmetric", "p_error": 0.1}, "seed": 1}
+
+
+def _cli(exe, *args, gpu=False, cwd=None):
+    env = dict(os.environ)
+    if not gpu:
+        env["CUDA_VISIBLE_DEVICES"] = ""
+    return subprocess.run([exe, *args], capture_output=True, text=True, timeout=600, env=env, cwd=cwd)
+
+
+def test_reference_cli_analyze_and_fit_identical_on_cpu(tmp_path):
+    """The host-only subcommands print the same bytes through both headers;
+    `analyze --batch-size 0` fails like the reference's CTest expects."""
+    ref, mine = _suite("binbatch_ref"), _suite("binbatch_b200")
+    args = ["analyze", "--batch-size", "128", "--k", "1,2,3,5", "--lambda", "10", "--epsilon", "0.1",
+            "--mu", "0.1"]
+    a, b = _cli(ref, *args), _cli(mine, *args)
+    assert a.returncode == 0 and b.returncode == 0, a.stderr + b.stderr
+    assert a.stdout == b.stdout and "max_throughput" in a.stdout
+    assert _cli(ref, "analyze", "--batch-size", "0").returncode != 0
+    assert _cli(mine, "analyze", "--batch-size", "0").returncode != 0
+    trace = tmp_path / "t.csv"
+    trace.write_text("id,token_count,measured_time\n" +
+                     "".join(f"{i},{10 + 7 * i},{0.5 + 0.03 * (10 + 7 * i) + 0.01 * (i % 3)}\n"
+                             for i in range(40)))
+    a, b = _cli(ref, "fit", "--trace", str(trace)), _cli(mine, "fit", "--trace", str(trace))
+    assert a.returncode == 0 and a.stdout == b.stdout, a.stderr + b.stderr
+
+
+@pytest.mark.gpu
+def test_reference_cli_simulate_sweep_compare_on_gpu(tmp_path):
+    """simulate / sweep / compare of the unchanged CLI on the B200 drop-in:
+    simulate equals the reference CLI (reference streams: exact fields
+    bit-equal, the Sigma-based ones within the reassociation bound); sweep
+    writes the reference's CSV shape and compare checks it against the
+    closed forms."""
+    import json
+    ref, mine = _suite("binbatch_ref"), _suite("binbatch_b200")
+    cfg = tmp_path / "run.json"
+    cfg.write_text(json.dumps(RUN_JSON))
+    a = _cli(ref, "simulate", "--config", str(cfg))
+    b = _cli(mine, "simulate", "--config", str(cfg), gpu=True)
+    assert a.returncode == 0 and b.returncode == 0, a.stderr + b.stderr
+    ja, jb = json.loads(a.stdout), json.loads(b.stdout)
+    for key in ("throughput", "makespan", "latency_p50", "latency_p99", "per_bin_batch_counts",
+                "n_completed", "seed"):
+        assert ja[key] == jb[key], key
+    for key in ("latency_mean", "server_busy_fraction"):
+        assert abs(ja[key] - jb[key]) <= 1e-12 * abs(ja[key]), key
+    spec = tmp_path / "spec.json"
+    base = {k: v for k, v in RUN_JSON.items() if k != "seed"}
+    base.update({"lambda": "inf"}, flush_partial=False, error={"type": "perfect"})
+    spec.write_text(json.dumps({"name": "capacity", "seed": 21, "replications": 10,
+                                "output": str(tmp_path / "capacity.csv"), "base": base,
+                                "sweep": [{"param": "k", "values": [1, 2, 3, 5]}]}))
+    r = _cli(mine, "sweep", "--spec", str(spec), gpu=True)
+    assert r.returncode == 0, r.stderr
+    rows = (tmp_path / "capacity.csv").read_text().splitlines()
+    assert len(rows) == 5 and rows[0].startswith("name,lambda,k,B,")
+    c = _cli(mine, "compare", "--results", str(tmp_path / "capacity.csv"), gpu=True)
+    assert c.returncode == 0, c.stdout + c.stderr  # Theorem 1 within the 2 % tolerance
+    assert "4 checks, 0 failures" in c.stdout
