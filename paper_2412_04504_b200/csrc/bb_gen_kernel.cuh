@@ -909,8 +909,30 @@ cudaError_t launch_mode_q(const GenLaunch& L, cudaStream_t s) {
   return L.timers ? launch_mode_qt<SVC, ERR, Q, true>(L, s) : launch_mode_qt<SVC, ERR, Q, false>(L, s);
 }
 
+#include "bb_genw_kernel.cuh"
+
+// Quantile mode with long replications: when the lane kernel's request logs
+// (14 B per request per lane) would not fit a full grid in HBM, one warp per
+// replication (bb_genw_kernel.cuh) keeps the grid full.  BB_WARP_MODE=0/1
+// forces the choice (tests; the results are identical either way).
+inline bool use_warp_mode(const GenLaunch& L) {
+  if (!L.quant || L.overload || L.s_max > 1 || L.timers || L.k_max > 32) return false;
+  static const int env = [] {
+    const char* v = getenv("BB_WARP_MODE");
+    return v ? (v[0] == '1' ? 1 : 0) : -1;
+  }();
+  if (env >= 0) return env == 1;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const uint64_t per_lane = (((uint64_t)L.n_max + 31) & ~31ull) * 14 + (uint64_t)L.nf_max * 8;
+  const uint64_t lanes = (uint64_t)sms * 2 * kGenThreads;  // the lane kernel's full grid
+  return per_lane * lanes > gen_scratch_budget();
+}
+
 template <int SVC, int ERR>
 cudaError_t launch_mode(const GenLaunch& L, cudaStream_t s) {
+  if (use_warp_mode(L)) return launch_genw<SVC, ERR>(L, s);
   return L.quant ? launch_mode_q<SVC, ERR, true>(L, s) : launch_mode_q<SVC, ERR, false>(L, s);
 }
 

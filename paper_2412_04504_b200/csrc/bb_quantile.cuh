@@ -80,13 +80,20 @@ constexpr uint32_t kQFStride = BB_QFSTRIDE;
 __host__ __device__ __forceinline__ size_t qlog_index(uint32_t i) {
   return (size_t)(i / kQRun) * (32 * kQRun) + (i % kQRun);
 }
+// the same with the distance between a replication's consecutive runs given:
+// 32 kQRun in the interleaved warp rows, kQRun in a replication's own
+// contiguous log (the warp-per-replication kernel, bb_genw_kernel.cuh)
+__host__ __device__ __forceinline__ size_t qlog_index(uint32_t i, uint32_t run_stride) {
+  return (size_t)(i / kQRun) * run_stride + (i % kQRun);
+}
 
 template <bool WRITE>
 struct QSrcLog {
-  double* A;            // the replication's first run (+ qlog_index(i))
+  double* A;            // the replication's first run (+ qlog_index(i, rs))
   const uint32_t* Id;   //   its batch ids, same layout
   const double* F;      // its completions by batch id
   uint32_t n, lane;
+  uint32_t rs = 32 * kQRun;  // run stride
 
   template <class Fn>
   __device__ void for_each(Fn&& f) const {
@@ -100,7 +107,7 @@ struct QSrcLog {
       for (int u = 0; u < kQChunk; ++u) {
         const uint32_t t = t0 + u;
         const bool v = t < nt && t * 32 + lane < n;
-        const size_t o = qlog_index(t * 32 + lane);
+        const size_t o = qlog_index(t * 32 + lane, rs);
         na[u] = v ? A[o] : 0.0;
         nid[u] = v ? Id[o] : 0xFFFFFFFFu;
       }
@@ -121,7 +128,7 @@ struct QSrcLog {
       for (int u = 0; u < kQChunk; ++u) {
         const double x = __dsub_rn(fin[u], a[u]);
         const uint32_t t = t0 + u;
-        if (WRITE && t < nt) A[qlog_index(t * 32 + lane)] = x;  // later passes read QSrcLat
+        if (WRITE && t < nt) A[qlog_index(t * 32 + lane, rs)] = x;  // later passes read QSrcLat
         f(x, isnan(x) ? 0u : 1u, t * 32 + lane);
       }
     }
@@ -186,11 +193,12 @@ struct QSrcBatches {
 // -- and keeps only the indices of requests in the wanted buckets; their
 // latencies are then gathered with independent loads.
 struct QFast {
-  uint16_t* Bk;         // the replication's buckets (+ qlog_index(i))
+  uint16_t* Bk;         // the replication's buckets (+ qlog_index(i, rs))
   const double* A;      // its arrivals
   const uint32_t* Id;   // its batch ids
   const double* F;      // its completions by batch id
   uint32_t n, lane;
+  uint32_t rs = 32 * kQRun;  // run stride
 
   // Level 0 of the selection in one lean pass over the log: every request's
   // latency F[id] - a (the reference's subtraction), their sum, a histogram
@@ -225,7 +233,7 @@ struct QFast {
 #define BB_QL0C 6
 #endif
     constexpr int C = BB_QL0C;
-    constexpr uint32_t R = 32 * kQRun;
+    const uint32_t R = rs;
     uint32_t t = 0;
     double a1[C], f1[C], a2[C];
     uint32_t i2[C];
@@ -264,7 +272,7 @@ struct QFast {
     }
     for (; t < nt; ++t) {
       const bool v = t * 32 + lane < n;
-      one(v ? a_p[t * (32 * kQRun)] : 0.0, v ? F[i_p[t * (32 * kQRun)]] : 0.0, v, t * (32 * kQRun));
+      one(v ? a_p[t * R] : 0.0, v ? F[i_p[t * R]] : 0.0, v, t * R);
     }
     return acc;
   }
@@ -286,7 +294,7 @@ struct QFast {
 #pragma unroll
       for (int u = 0; u < G; ++u) {
         const uint32_t g = g0 + u * 32 + lane;
-        v[u] = g < ng ? *reinterpret_cast<const uint4*>(Bk + qlog_index(g * 8))
+        v[u] = g < ng ? *reinterpret_cast<const uint4*>(Bk + qlog_index(g * 8, rs))
                       : make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
       }
 #pragma unroll
@@ -320,7 +328,7 @@ struct QFast {
     return nc;
   }
   __device__ double latency(uint32_t i) const {
-    const size_t o = qlog_index(i);
+    const size_t o = qlog_index(i, rs);
     return __dsub_rn(F[(size_t)Id[o] * kQFStride], A[o]);
   }
 };
