@@ -42,31 +42,48 @@ __device__ __forceinline__ double pow2i(int e) { return __longlong_as_double((lo
 // g >= 0 per lane (0 past the last request); t is warp-uniform and advanced.
 __device__ __forceinline__ double warp_clock(double& t, double g, uint32_t lane) {
   const int E = (int)((__double_as_longlong(t) >> 52) & 0x7FF) - 1023;
-  double tot = g;  // approximate step total (a bound is all that is needed)
-#pragma unroll
-  for (int o = 16; o; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
-  if (t > 0.0 && E > -960 && E < 960 && t + tot * (1.0 + 0x1.0p-40) + 64.0 * pow2i(E - 52) < pow2i(E + 1)) {
-    const double x = g * pow2i(52 - E);  // exact scaling: g < 2^(E+1)
+  if (t > 0.0 && E > -960 && E < 960) {
+    const double x = g * pow2i(52 - E);  // exact scaling
     const double qd = floor(x);
     const double f = x - qd;
     const long long q = (long long)qd;
-    const long long up = f > 0.5, half = f == 0.5;
-    long long i0 = q + up + (half & (q & 1)), i1 = q + up + (half & ((q + 1) & 1));
+    const bool up = f > 0.5, half = f == 0.5;
+    const long long a = (long long)(t * pow2i(52 - E));  // t = a u, a in [2^52, 2^53)
+    long long i0 = q + up;
+    if (!__any_sync(0xffffffffu, half)) {
+      // no exact tie: the increments do not depend on parity -- a plain sum
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {  // inclusive scan: (earlier) then (mine)
-      const long long j0 = __shfl_up_sync(0xffffffffu, i0, o), j1 = __shfl_up_sync(0xffffffffu, i1, o);
-      if (lane >= (uint32_t)o) {
-        const long long n0 = j0 + ((j0 & 1) ? i1 : i0), n1 = j1 + ((j1 & 1) ? i0 : i1);
-        i0 = n0;
-        i1 = n1;
+      for (int o = 1; o < 32; o <<= 1) {
+        const long long j = __shfl_up_sync(0xffffffffu, i0, o);
+        if (lane >= (uint32_t)o) i0 += j;
+      }
+      const long long end = a + __shfl_sync(0xffffffffu, i0, 31);
+      if (end < (1ll << 53)) {  // (monotone: every partial sum stays in the binade)
+        const double ti = (double)(a + i0) * pow2i(E - 52);
+        t = (double)end * pow2i(E - 52);
+        return ti;
+      }
+    } else {
+      long long i1 = i0 + (half & ((q + 1) & 1));
+      i0 += half & (q & 1);
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {  // inclusive scan: (earlier) then (mine)
+        const long long j0 = __shfl_up_sync(0xffffffffu, i0, o), j1 = __shfl_up_sync(0xffffffffu, i1, o);
+        if (lane >= (uint32_t)o) {
+          const long long n0 = j0 + ((j0 & 1) ? i1 : i0), n1 = j1 + ((j1 & 1) ? i0 : i1);
+          i0 = n0;
+          i1 = n1;
+        }
+      }
+      const long long mine = a + ((a & 1) ? i1 : i0);
+      const long long end = __shfl_sync(0xffffffffu, mine, 31);
+      if (__all_sync(0xffffffffu, x < 0x1.0p52) && end < (1ll << 53)) {
+        t = (double)end * pow2i(E - 52);
+        return (double)mine * pow2i(E - 52);
       }
     }
-    const long long a = (long long)(t * pow2i(52 - E));
-    const double ti = (double)(a + ((a & 1) ? i1 : i0)) * pow2i(E - 52);
-    t = __shfl_sync(0xffffffffu, ti, 31);
-    return ti;
   }
-  double ti = 0.0;
+  double ti = 0.0;  // the first step (t = 0), a binade crossing: the serial chain
 #pragma unroll 8
   for (int l = 0; l < 32; ++l) {
     t = __dadd_rn(t, __shfl_sync(0xffffffffu, g, l));
