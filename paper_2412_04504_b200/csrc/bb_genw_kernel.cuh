@@ -291,7 +291,8 @@ __global__ void __launch_bounds__(kGenThreads, 2) genw_kernel(const __grid_const
         src.rs = kQRun;
         QFast qf{logK, logA, logI, logF, n, lane};
         qf.rs = kQRun;
-        q_select(src, src, ncomp, lmin, lmax, wreg, kWRegion, q_ans, lane, v50, v99, &sum, &qf);
+        q_select<QSrcLog<false>, QSrcLog<false>, true>(src, src, ncomp, lmin, lmax, wreg, kWRegion, q_ans, lane,
+                                                       v50, v99, &sum, &qf);
         lat_out = sum / (double)ncomp;
         q_p50 = v50;
         q_p99 = v99;

@@ -333,12 +333,54 @@ struct QFast {
   }
 };
 
+// Later passes of the request log, reading only the requests whose level-0
+// bucket is one of want[0..3] (every open target lies inside its level-0
+// bucket): a scan of the 2-byte bucket ids, the latency recomputed for the
+// few hits.  f is called by all lanes in lockstep (weight 0 for no element),
+// once per row of eight buckets in which some lane has a hit.
+struct QBkSrc {
+  const QFast* qf;
+  uint32_t want[4];
+
+  template <class Fn>
+  __device__ void for_each(Fn&& f) const {
+    const uint32_t n = qf->n, lane = qf->lane;
+    const uint32_t ng = (n + 7) / 8;
+    for (uint32_t g0 = 0; g0 < ng; g0 += 32) {
+      const uint32_t g = g0 + lane;
+      const uint4 v = g < ng ? *reinterpret_cast<const uint4*>(qf->Bk + qlog_index(g * 8, qf->rs))
+                             : make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+      uint32_t hm = 0;
+#pragma unroll
+      for (int h = 0; h < 8; ++h) {
+        const uint32_t bk = (w[h >> 1] >> (16 * (h & 1))) & 0xFFFFu;
+        hm |= (uint32_t)(bk == want[0] || bk == want[1] || bk == want[2] || bk == want[3]) << h;
+      }
+      const uint32_t base = g * 8;
+      if (base + 8 > n) hm &= base < n ? (1u << (n - base)) - 1u : 0u;
+      uint32_t rows = __reduce_or_sync(kQFull, hm);
+      while (rows) {
+        const int h = __ffs(rows) - 1;
+        rows &= rows - 1;
+        const bool hit = (hm >> h) & 1u;
+        const double x = hit ? qf->latency(base + h) : 0.0;
+        f(x, hit ? 1u : 0u, base + h);
+      }
+    }
+  }
+};
+
 // Exact p50 and p99 (interpolated_quantile, binning.hpp:97-104) of the
 // multiset produced by `src` (m = total weight, every value in [lmin, lmax],
 // all positive).  Warp-collective; results are warp-uniform.
 // region: >= kQRegionMin bytes of shared memory (histogram, then candidates);
 // ans: 4 doubles of shared memory.
-template <class Src1, class Src>
+// BK: the slow path (targets' level-0 buckets too full for shared memory)
+// re-reads only the requests of those buckets through their bucket ids
+// (QBkSrc) instead of the whole log -- the long replications of the warp
+// kernel reach it often; the lane kernel rarely does and keeps its registers
+template <class Src1, class Src, bool BK = false>
 __device__ void q_select(Src1& first, const Src& src, uint64_t m, double lmin, double lmax, unsigned char* region,
                          uint32_t region_bytes, double* ans, uint32_t lane, double& p50,
                          double& p99, double* wsum, const QFast* qf = nullptr) {
@@ -434,6 +476,7 @@ __device__ void q_select(Src1& first, const Src& src, uint64_t m, double lmin, d
   };
 
   uint32_t hb = 0, hs = 0;  // request log: level-0 buckets over the keys' high words
+  QBkSrc bksrc{qf, {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu}};
   if (qf) {
     hb = (uint32_t)(kbase >> 32);
     const uint32_t hspan = (uint32_t)(qkey(lmax) >> 32) - hb;
@@ -473,6 +516,7 @@ __device__ void q_select(Src1& first, const Src& src, uint64_t m, double lmin, d
         }
       }
       b = __shfl_sync(kQFull, b, who);
+      if constexpr (BK) bksrc.want[t] = b;
       klo[t] = (uint64_t)(hb + (b << hs)) << 32;
       sh[t] = hs + 32;
       below[t] = __shfl_sync(kQFull, c, who);
@@ -535,7 +579,12 @@ __device__ void q_select(Src1& first, const Src& src, uint64_t m, double lmin, d
 #pragma unroll
     for (int t = 0; t < 4; ++t)
       if (t == big) glo = klo[t], gsh = sh[t];
-    refine(src, glo, gsh, false);
+    if constexpr (BK) {
+      if (qf) refine(bksrc, glo, gsh, false);  // (only the targets' level-0 buckets)
+      else refine(src, glo, gsh, false);
+    } else {
+      refine(src, glo, gsh, false);
+    }
   }
 
   bool open = false;
@@ -550,7 +599,7 @@ __device__ void q_select(Src1& first, const Src& src, uint64_t m, double lmin, d
       wlo[t] = klo[t];
       ww[t] = done[t] ? 0ull : qwidth(sh[t]);
     }
-    if (!fast) src.for_each([&](double x, uint32_t w, uint32_t) {
+    auto keep = [&](double x, uint32_t w, uint32_t) {
       const uint64_t key = qkey(x);
       bool hit = false;
 #pragma unroll
@@ -565,7 +614,15 @@ __device__ void q_select(Src1& first, const Src& src, uint64_t m, double lmin, d
         }
       }
       nc += __popc(hm);
-    });
+    };
+    if (!fast) {
+      if constexpr (BK) {
+        if (qf) bksrc.for_each(keep);  // (only the targets' level-0 buckets)
+        else src.for_each(keep);
+      } else {
+        src.for_each(keep);
+      }
+    }
     if (nc > cap) nc = cap;  // cannot happen: the ranges were refined to fit
     __syncwarp();
     // resolve each open rank among the candidates: 256-bucket histograms of
