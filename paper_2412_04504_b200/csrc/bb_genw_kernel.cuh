@@ -93,7 +93,7 @@ __device__ __forceinline__ double warp_clock(double& t, double g, uint32_t lane)
 }
 
 __host__ __device__ __forceinline__ uint32_t genw_warp_bytes() {
-  return kWRegion + 64 + 3 * 32 * 4 + 32 * 8 + 2 * 64 * 4;
+  return kWRegion + 64 + 3 * 32 * 4 + 32 * 8 + 2 * 64 * 4 + 32 * 8;
 }
 
 template <int SVC, int ERR>
@@ -114,6 +114,7 @@ __global__ void __launch_bounds__(kGenThreads, 2) genw_kernel(const __grid_const
   uint64_t* s_nkey = reinterpret_cast<uint64_t*>(wreg + kWRegion + 64 + 3 * 32 * 4);  // ... its max key
   uint32_t* s_shi = reinterpret_cast<uint32_t*>(s_nkey + 32);  // [64] batch maxima of a step: high words
   uint32_t* s_slo = s_shi + 64;                                 //   ... low words
+  double* s_nprev = reinterpret_cast<double*>(s_slo + 64);      // per bin: its last closing time
 
   const uint32_t nrep = L.rep_end - L.rep_begin;
   const uint64_t n_items = (uint64_t)nrep * L.n_points;
@@ -222,37 +223,44 @@ __global__ void __launch_bounds__(kGenThreads, 2) genw_kernel(const __grid_const
         logA[i] = ti;
         logI[i] = myid;
       }
-      // closings in request order: the Lindley step and the batch's completion
-      uint32_t cm = __ballot_sync(kQFull, closing);
-      while (cm) {
-        const int c = __ffs(cm) - 1;
-        cm &= cm - 1;
-        const double Rt = __shfl_sync(kQFull, ti, c);
-        const uint64_t kc = __shfl_sync(kQFull, bkey, c);
-        const uint32_t idc = __shfl_sync(kQFull, myid, c);
-        const uint32_t bc = __shfl_sync(kQFull, pb, c) - 1;
-        const double S = svc_of_key_t<SVC>(svc, kc);
-        const double fin = D = __dadd_rn(fmax(D, Rt), S);
-        busy += S;
-        ncomp += B;
-        const double prev = __shfl_sync(kQFull, oprev, bc);
-        const double lo = __dsub_rn(fin, Rt), hi = __dsub_rn(fin, prev);
+      // closings: every closing batch's service at once (one pass however
+      // many close), then the Lindley chain in request order
+      const uint32_t cm = __ballot_sync(kQFull, closing);
+      double S = 0.0, fin = 0.0;
+      if (closing) S = svc_of_key_t<SVC>(svc, bkey);
+      for (uint32_t m = cm; m; m &= m - 1) {
+        const int c = __ffs(m) - 1;
+        D = __dadd_rn(fmax(D, __shfl_sync(kQFull, ti, c)), __shfl_sync(kQFull, S, c));
+        busy += __shfl_sync(kQFull, S, c);
+        if (lane == (uint32_t)c) fin = D;
+      }
+      ncomp += (uint64_t)B * __popc(cm);
+      // the bin's previous closing: an earlier closing lane of the bin, else carried
+      const uint32_t ecl = cm & peers & lt;
+      const double prev_e = __shfl_sync(kQFull, ti, ecl ? 31 - __clz(ecl) : lane);
+      const double prev_c = __shfl_sync(kQFull, oprev, pb ? pb - 1 : 0);
+      if (closing) {
+        logF[myid] = fin;
+        const double lo = __dsub_rn(fin, ti), hi = __dsub_rn(fin, ecl ? prev_e : prev_c);
         lmin = lo < lmin ? lo : lmin;  // the closing member: the batch's smallest latency
         lmax = hi > lmax ? hi : lmax;  // bounds the first member's (it arrived later)
-        if (lane == bc) oprev = Rt;
-        if (lane == 0) logF[idc] = fin;
       }
-      // carry each bin's open batch to the next step (its last member knows it)
+      // carry each bin's open batch (its last member) and last closing time to the next step
       s_seen[lane] = 0;
       __syncwarp();
       if (pb && (peers >> lane) == 1u) {  // the bin's highest lane this step
         s_ncnt[pb - 1] = closing ? 0u : within + 1;
         s_nid[pb - 1] = myid;
         s_nkey[pb - 1] = closing ? 0ull : bkey;
-        s_seen[pb - 1] = 1;
+        atomicOr(&s_seen[pb - 1], 1u);
+      }
+      if (closing && !(cm & peers & ~lt & ~(1u << lane))) {  // the bin's last closing this step
+        s_nprev[pb - 1] = ti;
+        atomicOr(&s_seen[pb - 1], 2u);
       }
       __syncwarp();
-      if (lane < k && s_seen[lane]) {
+      if (lane < k && (s_seen[lane] & 2)) oprev = s_nprev[lane];
+      if (lane < k && (s_seen[lane] & 1)) {
         cnt = s_ncnt[lane];
         oid = s_nid[lane];
         okey = s_nkey[lane];
@@ -261,6 +269,11 @@ __global__ void __launch_bounds__(kGenThreads, 2) genw_kernel(const __grid_const
     }
     double mk_out = 0.0, thr_out = 0.0, busy_out = 0.0, lat_out = 0.0;
     double q_p50 = BB_QNAN, q_p99 = BB_QNAN;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {  // the closing lanes' latency bounds
+      lmin = fmin(lmin, __shfl_xor_sync(kQFull, lmin, o));
+      lmax = fmax(lmax, __shfl_xor_sync(kQFull, lmax, o));
+    }
     if (!failed) {
       // after the last arrival: on_drain partials in bin order (simulator.hpp:203-205,218-221),
       // or leftovers that never complete (no flush)
