@@ -1267,6 +1267,94 @@ __global__ void binade_fill_kernel(const double* __restrict__ S, const double* _
   finish[d] = ldexp((double)ad, e - 52);
 }
 
+// the last value of a device-counted array (0 when empty)
+__global__ void last_of_kernel(const double* v, const uint32_t* nbp, double* out) {
+  const uint32_t nb = *nbp;
+  *out = nb ? v[nb - 1] : 0.0;
+}
+
+// --------------------------------- multi-server dispatch, chunk-parallel
+// S > 1 servers (simulator.hpp:256-277): the central queue is FIFO, so batch
+// i starts on the earliest-free server, start_i = max(R_i, min_j V_j), and
+// that server's free time becomes finish_i = fl(start_i + S_i) (the
+// Kiefer-Wolfowitz recursion; a server freed at R_i is idle for a batch
+// formed at R_i because batch_done events rank first, :108-114).
+// Kiefer-Wolfowitz in parallel: the batches split into chunks of KWP_CH;
+// each chunk is first dispatched from an all-idle server state
+// (kw_spec_kernel, one thread per chunk, its heap of S free times in global
+// scratch).  That speculation is exact whenever every server is free at the
+// chunk's first formation time: free times <= R_first stay <= every later R
+// (R is non-decreasing in dispatch order), so they act exactly like -inf in
+// start = max(R, min free).  kw_fix_kernel walks the chunks in order with
+// the true incoming state and re-dispatches (serially, from that state) only
+// the chunks whose check fails -- light load runs in parallel, heavy load
+// degrades to the serial recursion.  The busy time (a sequential fp64 sum
+// in dispatch order, simulator.hpp:263) comes from the exact Lindley
+// pipeline run on (R = 0, S) (D_n = S_1 + ... + S_n in order).
+constexpr uint32_t KWP_CH = 1024;
+
+__device__ __forceinline__ void kw_run(const double* __restrict__ R, const double* __restrict__ S, uint32_t lo,
+                                       uint32_t hi, double* heap, uint32_t nsrv, double* __restrict__ start,
+                                       double* __restrict__ finish, double& last) {
+  for (uint32_t j = lo; j < hi; ++j) {
+    const double st = fmax(heap[0], R[j]);
+    const double f = __dadd_rn(st, S[j]);
+    start[j] = st;
+    finish[j] = f;
+    last = fmax(last, f);
+    uint32_t h = 0;  // replace the minimum by f (f >= old minimum) and sift down
+    for (;;) {
+      uint32_t c = 2 * h + 1;
+      if (c >= nsrv) break;
+      if (c + 1 < nsrv && heap[c + 1] < heap[c]) ++c;
+      if (!(heap[c] < f)) break;
+      heap[h] = heap[c];
+      h = c;
+    }
+    heap[h] = f;
+  }
+}
+
+__global__ void kw_spec_kernel(const double* __restrict__ R, const double* __restrict__ S, const uint32_t* nbp,
+                               uint32_t nsrv, double* heaps, double* __restrict__ start,
+                               double* __restrict__ finish, double* chunk_last) {
+  const uint32_t nb = *nbp, g = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t lo = g * KWP_CH;
+  if (lo >= nb) return;
+  double* heap = heaps + (size_t)g * nsrv;
+  for (uint32_t q = 0; q < nsrv; ++q) heap[q] = -CUDART_INF;  // all idle
+  double last = 0.0;
+  kw_run(R, S, lo, min(nb, lo + KWP_CH), heap, nsrv, start, finish, last);
+  chunk_last[g] = last;
+}
+
+__global__ void kw_fix_kernel(const double* __restrict__ R, const double* __restrict__ S, const uint32_t* nbp,
+                              uint32_t nsrv, double* heaps, double* __restrict__ start,
+                              double* __restrict__ finish, double* chunk_last, double* last_out,
+                              uint32_t* refixed) {
+  if (threadIdx.x != 0) return;
+  const uint32_t nb = *nbp, G = (nb + KWP_CH - 1) / KWP_CH;
+  double last = G ? chunk_last[0] : 0.0, in_max = last;  // (the state's max free time)
+  uint32_t fixed = 0;
+  for (uint32_t g = 1; g < G; ++g) {
+    const uint32_t lo = g * KWP_CH;
+    if (!(in_max <= R[lo])) {  // a server still busy at the chunk's first formation
+      double* heap = heaps + (size_t)g * nsrv;
+      const double* prev = heaps + (size_t)(g - 1) * nsrv;
+      for (uint32_t q = 0; q < nsrv; ++q) heap[q] = prev[q];  // the true incoming state
+      double cl = 0.0;
+      kw_run(R, S, lo, min(nb, lo + KWP_CH), heap, nsrv, start, finish, cl);
+      chunk_last[g] = cl;
+      ++fixed;
+    }
+    // the outgoing state's max: the largest free time (>= the previous max)
+    in_max = fmax(in_max, chunk_last[g]);
+    last = fmax(last, chunk_last[g]);
+  }
+  *last_out = last;
+  *refixed = fixed;
+}
+
 // ------------------------------------------------------------- requests
 struct QArgs {
   const double* a;
@@ -1286,70 +1374,6 @@ struct QArgs {
   uint32_t* members;
 };
 
-// ------------------------------------------------ multi-server dispatch
-// S > 1 servers (simulator.hpp:256-277): the central queue is FIFO, so batch
-// i starts on the earliest-free server, start_i = max(R_i, min_j V_j), and
-// that server's free time becomes finish_i = fl(start_i + S_i) (the
-// Kiefer-Wolfowitz recursion; a server freed at R_i is idle for a batch
-// formed at R_i because batch_done events rank first, :108-114).  One block:
-// all threads stage chunks of (R, S) in shared memory, thread 0 runs the
-// recursion over a binary min-heap of free times (shared memory up to
-// KW_HEAP servers), the block writes (start, finish) back.  busy_time_ and
-// last_completion_ accumulate in dispatch order, as the reference does.
-constexpr uint32_t KW_CH = 1024, KW_HEAP = 2048;
-__global__ void __launch_bounds__(256) kw_dispatch_kernel(const double* __restrict__ R,
-                                                          const double* __restrict__ S, const uint32_t* nbp,
-                                                          uint32_t nsrv, double* heap_g,
-                                                          double* __restrict__ start,
-                                                          double* __restrict__ finish,
-                                                          double* busy_out, double* last_out) {
-  __shared__ double sA[KW_CH], sB[KW_CH];  // (R, S) in, (start, finish) out
-  __shared__ double sheap[KW_HEAP];
-  double* heap = nsrv <= KW_HEAP ? sheap : heap_g;
-  const uint32_t nb = *nbp;
-  for (uint32_t i = threadIdx.x; i < nsrv; i += blockDim.x) heap[i] = -CUDART_INF;  // all idle
-  double busy = 0.0, last = 0.0;
-  for (uint32_t base = 0; base < nb; base += KW_CH) {
-    const uint32_t m = min(KW_CH, nb - base);
-    __syncthreads();
-    for (uint32_t j = threadIdx.x; j < m; j += blockDim.x) {
-      sA[j] = R[base + j];
-      sB[j] = S[base + j];
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      for (uint32_t j = 0; j < m; ++j) {
-        const double sv = sB[j];
-        const double st = fmax(heap[0], sA[j]);
-        const double f = __dadd_rn(st, sv);
-        sA[j] = st;
-        sB[j] = f;
-        busy = __dadd_rn(busy, sv);
-        last = fmax(last, f);
-        // replace the minimum by f (f >= old minimum) and sift down
-        uint32_t h = 0;
-        for (;;) {
-          uint32_t c = 2 * h + 1;
-          if (c >= nsrv) break;
-          if (c + 1 < nsrv && heap[c + 1] < heap[c]) ++c;
-          if (!(heap[c] < f)) break;
-          heap[h] = heap[c];
-          h = c;
-        }
-        heap[h] = f;
-      }
-    }
-    __syncthreads();
-    for (uint32_t j = threadIdx.x; j < m; j += blockDim.x) {
-      start[base + j] = sA[j];
-      finish[base + j] = sB[j];
-    }
-  }
-  if (threadIdx.x == 0) {
-    *busy_out = busy;
-    *last_out = last;
-  }
-}
 
 constexpr int RQ_T = 256, RQ_E = 4;  // request pass: threads, requests per thread
 __global__ void __launch_bounds__(RQ_T) request_kernel(QArgs Q) {
@@ -2445,39 +2469,47 @@ void trace_run(const TraceArgs& A, TraceResult* R, cudaStream_t s) {
     BB_CK(pool.alloc((void**)&busy_sum, 8));
     BB_CK(pool.alloc((void**)&last_dev, 8));
     BB_CK(cudaMemsetAsync(last_dev, 0, 8, s));
-    if (A.n_servers > 1) {  // S servers: Kiefer-Wolfowitz, dispatch order
-      double* heap_g = nullptr;
-      if (A.n_servers > KW_HEAP) BB_CK(pool.alloc((void**)&heap_g, (size_t)A.n_servers * 8));
-      kw_dispatch_kernel<<<1, 256, 0, s>>>(dR, dS, nbp, A.n_servers, heap_g, start, finish, busy_sum,
-                                           last_dev);
-      note_launch();
-      BB_CK(cudaGetLastError());
-    } else {
+    // the exact Lindley recursion D = fl(max(D, R) + S) over (R, S) in
+    // dispatch order into (st, fn): max-plus scan, certified busy-period
+    // splits, binade parity scan, serial segments only as a fallback
+    auto exact_lindley = [&](const double* dRl, const double* dSl, double* st, double* fn,
+                             double** busy_part_out) -> cudaError_t {
+      const double* dR = dRl;
+      const double* dS = dSl;
+      double* start = st;
+      double* finish = fn;
+      cudaError_t e_ = cudaSuccess;
+#define BB_LCK(x)                             \
+  do {                                        \
+    if ((e_ = (x)) != cudaSuccess) return e_; \
+  } while (0)
+      BB_LCK(cudaMemsetAsync(ws.counters + 1, 0, 8, s));  // the scans' tile tickets
       // Lindley: certified busy-period splits, then exact serial segments
       const uint32_t lt = nb ? (nb + LTILE - 1) / LTILE : 1;
       double *aggA, *aggC, *incA, *incC, *busy_part;
+      (void)dR;
       uint32_t* lflag;
-      BB_CK(pool.alloc((void**)&aggA, (size_t)lt * 8));
-      BB_CK(pool.alloc((void**)&aggC, (size_t)lt * 8));
-      BB_CK(pool.alloc((void**)&incA, (size_t)lt * 8));
-      BB_CK(pool.alloc((void**)&incC, (size_t)lt * 8));
-      BB_CK(pool.alloc((void**)&busy_part, (size_t)lt * 8));
-      BB_CK(pool.alloc((void**)&lflag, (size_t)lt * 4));
-      BB_CK(cudaMemsetAsync(lflag, 0, (size_t)lt * 4, s));
+      BB_LCK(pool.alloc((void**)&aggA, (size_t)lt * 8));
+      BB_LCK(pool.alloc((void**)&aggC, (size_t)lt * 8));
+      BB_LCK(pool.alloc((void**)&incA, (size_t)lt * 8));
+      BB_LCK(pool.alloc((void**)&incC, (size_t)lt * 8));
+      BB_LCK(pool.alloc((void**)&busy_part, (size_t)lt * 8));
+      BB_LCK(pool.alloc((void**)&lflag, (size_t)lt * 4));
+      BB_LCK(cudaMemsetAsync(lflag, 0, (size_t)lt * 4, s));
       const double tol_rel = (double)(nb + 4096) * 0x1.0p-50;
       double* Dt;
-      BB_CK(pool.alloc((void**)&Dt, (size_t)nb * 8 + 8));
+      BB_LCK(pool.alloc((void**)&Dt, (size_t)nb * 8 + 8));
       {
         LArgs L{dR, dS, nbp, split, Dt, busy_part, aggA, aggC, incA, incC, lflag, ws.counters + 1,
                 tol_rel};
         if (nb) lindley_scan_kernel<<<lt, LB, 0, s>>>(L);
         note_launch();
-        BB_CK(cudaGetLastError());
+        BB_LCK(cudaGetLastError());
       }
       // exact values: binade parity scan (parallel), serial segments only as a fallback
       int* bad;
-      BB_CK(pool.alloc((void**)&bad, 4));
-      BB_CK(cudaMemsetAsync(bad, 0, 4, s));
+      BB_LCK(pool.alloc((void**)&bad, 4));
+      BB_LCK(cudaMemsetAsync(bad, 0, 4, s));
       if (nb) {
         BArgs Bq{};
         Bq.R = dR;
@@ -2486,38 +2518,75 @@ void trace_run(const TraceArgs& A, TraceResult* R, cudaStream_t s) {
         Bq.code = split;
         Bq.nbp = nbp;
         Bq.tol_rel = tol_rel;
-        BB_CK(pool.alloc((void**)&Bq.p0, (size_t)nb * 8));
-        BB_CK(pool.alloc((void**)&Bq.p1, (size_t)nb * 8));
-        BB_CK(pool.alloc((void**)&Bq.head_of, (size_t)nb * 4));
-        BB_CK(pool.alloc((void**)&Bq.run_last, (size_t)nb * 4));
-        BB_CK(pool.alloc((void**)&Bq.run_info, (size_t)nb * sizeof(RunInfo)));
-        BB_CK(pool.alloc((void**)&Bq.ag0, (size_t)lt * 8));
-        BB_CK(pool.alloc((void**)&Bq.ag1, (size_t)lt * 8));
-        BB_CK(pool.alloc((void**)&Bq.in0, (size_t)lt * 8));
-        BB_CK(pool.alloc((void**)&Bq.in1, (size_t)lt * 8));
-        BB_CK(pool.alloc((void**)&Bq.agh, (size_t)lt * 4));
-        BB_CK(pool.alloc((void**)&Bq.inh, (size_t)lt * 4));
-        BB_CK(pool.alloc((void**)&Bq.agf, (size_t)lt * 4));
-        BB_CK(pool.alloc((void**)&Bq.inf, (size_t)lt * 4));
-        BB_CK(pool.alloc((void**)&Bq.flag, (size_t)lt * 4));
-        BB_CK(cudaMemsetAsync(Bq.flag, 0, (size_t)lt * 4, s));
+        BB_LCK(pool.alloc((void**)&Bq.p0, (size_t)nb * 8));
+        BB_LCK(pool.alloc((void**)&Bq.p1, (size_t)nb * 8));
+        BB_LCK(pool.alloc((void**)&Bq.head_of, (size_t)nb * 4));
+        BB_LCK(pool.alloc((void**)&Bq.run_last, (size_t)nb * 4));
+        BB_LCK(pool.alloc((void**)&Bq.run_info, (size_t)nb * sizeof(RunInfo)));
+        BB_LCK(pool.alloc((void**)&Bq.ag0, (size_t)lt * 8));
+        BB_LCK(pool.alloc((void**)&Bq.ag1, (size_t)lt * 8));
+        BB_LCK(pool.alloc((void**)&Bq.in0, (size_t)lt * 8));
+        BB_LCK(pool.alloc((void**)&Bq.in1, (size_t)lt * 8));
+        BB_LCK(pool.alloc((void**)&Bq.agh, (size_t)lt * 4));
+        BB_LCK(pool.alloc((void**)&Bq.inh, (size_t)lt * 4));
+        BB_LCK(pool.alloc((void**)&Bq.agf, (size_t)lt * 4));
+        BB_LCK(pool.alloc((void**)&Bq.inf, (size_t)lt * 4));
+        BB_LCK(pool.alloc((void**)&Bq.flag, (size_t)lt * 4));
+        BB_LCK(cudaMemsetAsync(Bq.flag, 0, (size_t)lt * 4, s));
         Bq.counter = ws.counters + 2;
         binade_scan_kernel<<<lt, LB, 0, s>>>(Bq);
         note_launch();
-        BB_CK(cudaGetLastError());
+        BB_LCK(cudaGetLastError());
         binade_chain_kernel<<<grid_for(nb, 128), 128, 0, s>>>(dR, dS, Dt, split, Bq.p0, Bq.p1,
                                                               Bq.run_info, nbp, start, finish, bad);
         note_launch();
-        BB_CK(cudaGetLastError());
+        BB_LCK(cudaGetLastError());
         binade_fill_kernel<<<grid_for(nb, 256), 256, 0, s>>>(dS, Dt, split, Bq.p0, Bq.p1, Bq.head_of,
                                                              nbp, tol_rel, start, finish, bad);
         note_launch();
-        BB_CK(cudaGetLastError());
+        BB_LCK(cudaGetLastError());
         lindley_segments_kernel<<<grid_for(nb, 128), 128, 0, s>>>(dR, dS, split, nbp, start, finish, bad);
         note_launch();
-        BB_CK(cudaGetLastError());
+        BB_LCK(cudaGetLastError());
       }
-      sum_kernel<<<1, 256, 0, s>>>(busy_part, 0, busy_sum, nbp);
+      *busy_part_out = busy_part;
+#undef BB_LCK
+      return cudaSuccess;
+    };
+    if (A.n_servers > 1) {  // S servers: Kiefer-Wolfowitz in dispatch order, chunk-parallel
+      const uint32_t G = nb / KWP_CH + 1;
+      double *heaps, *chunk_last, *zeros, *bst, *bfn;
+      uint32_t* refixed;
+      BB_CK(pool.alloc((void**)&heaps, (size_t)G * A.n_servers * 8));
+      BB_CK(pool.alloc((void**)&chunk_last, (size_t)G * 8));
+      BB_CK(pool.alloc((void**)&refixed, 4));
+      kw_spec_kernel<<<grid_for(G, 128), 128, 0, s>>>(dR, dS, nbp, A.n_servers, heaps, start, finish,
+                                                      chunk_last);
+      kw_fix_kernel<<<1, 32, 0, s>>>(dR, dS, nbp, A.n_servers, heaps, start, finish, chunk_last, last_dev,
+                                     refixed);
+      note_launch(2);
+      BB_CK(cudaGetLastError());
+      // busy time: the sequential sum of the services in dispatch order, exactly
+      BB_CK(pool.alloc((void**)&zeros, (size_t)nb * 8 + 8));
+      BB_CK(pool.alloc((void**)&bst, (size_t)nb * 8 + 8));
+      BB_CK(pool.alloc((void**)&bfn, (size_t)nb * 8 + 8));
+      BB_CK(cudaMemsetAsync(zeros, 0, (size_t)nb * 8 + 8, s));
+      double* bp = nullptr;
+      if (nb) {
+        cudaError_t el = exact_lindley(zeros, dS, bst, bfn, &bp);
+        if (el != cudaSuccess) BB_CK(el);
+      }
+      last_of_kernel<<<1, 1, 0, s>>>(bfn, nbp, busy_sum);
+      note_launch();
+      BB_CK(cudaGetLastError());
+    } else {
+      double* busy_part = nullptr;
+      if (nb) {
+        cudaError_t el = exact_lindley(dR, dS, start, finish, &busy_part);
+        if (el != cudaSuccess) BB_CK(el);
+      }
+      if (busy_part) sum_kernel<<<1, 256, 0, s>>>(busy_part, 0, busy_sum, nbp);
+      else BB_CK(cudaMemsetAsync(busy_sum, 0, 8, s));
       note_launch();
       BB_CK(cudaGetLastError());
     }

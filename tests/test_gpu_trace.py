@@ -231,3 +231,25 @@ def test_full_size_c2_trace_bit_exact():
     check_against(res, exp, cfg["n_requests"])
     lat = d["req_completion"] - d["req_arrival"]
     check_metrics(res.metrics, m, cfg["n_requests"], np.nansum(np.abs(lat)), d["bat_service"].sum())
+
+
+@pytest.mark.parametrize("servers,load", [(4, 0.5), (4, 1.3), (64, 0.6), (3, 0.99)])
+def test_multi_server_chunk_parallel_dispatch_bit_exact(servers, load):
+    """Kiefer-Wolfowitz dispatch over ~1e5 batches (chunks of 1024 dispatched
+    from an all-idle state, re-dispatched serially where a server is still
+    busy at the chunk's first formation): start/finish, completions and the
+    busy fraction (the sequential busy-time sum) bit-identical to the oracle,
+    in light load (most chunks speculative) and overload (all re-dispatched)."""
+    n, B, k = 1_600_000, 16, 4
+    cap = servers * bb.throughput(B, k, 1.0, 20.0)
+    cfg = dict(arrival_rate=load * cap, n_requests=n, batch_size=B,
+               edges=bb.uniform_boundaries(k, 1.0, 20.0).edges, lo=1.0, hi=20.0, seed=4242 + servers,
+               n_servers=servers)
+    m, d, u, exp = oracle_case(cfg)
+    c = sim_config(cfg)
+    c.n_servers = servers
+    res = bb.run_trace(c, d["req_arrival"], d["req_service"], detailed=True)
+    check_against(res, exp, n)
+    assert same_bits(res.metrics.makespan, m["makespan"])
+    assert same_bits(res.metrics.server_busy_fraction, m["server_busy_fraction"])
+    assert same_bits(res.metrics.latency_p99, m["latency_p99"])
