@@ -1293,12 +1293,12 @@ __global__ void last_of_kernel(const double* v, const uint32_t* nbp, double* out
 // pipeline run on (R = 0, S) (D_n = S_1 + ... + S_n in order).
 constexpr uint32_t KWP_CH = 1024;
 
-__device__ __forceinline__ void kw_run(const double* __restrict__ R, const double* __restrict__ S, uint32_t lo,
-                                       uint32_t hi, double* heap, uint32_t nsrv, double* __restrict__ start,
-                                       double* __restrict__ finish, double& last) {
+__device__ __forceinline__ void kw_run(const double* R, const double* S, uint32_t lo, uint32_t hi, double* heap,
+                                       uint32_t nsrv, double* start, double* finish, double& last) {
   for (uint32_t j = lo; j < hi; ++j) {
-    const double st = fmax(heap[0], R[j]);
-    const double f = __dadd_rn(st, S[j]);
+    const double r = R[j], sv = S[j];  // (read before the in-place writes)
+    const double st = fmax(heap[0], r);
+    const double f = __dadd_rn(st, sv);
     start[j] = st;
     finish[j] = f;
     last = fmax(last, f);
@@ -1328,31 +1328,55 @@ __global__ void kw_spec_kernel(const double* __restrict__ R, const double* __res
   chunk_last[g] = last;
 }
 
-__global__ void kw_fix_kernel(const double* __restrict__ R, const double* __restrict__ S, const uint32_t* nbp,
-                              uint32_t nsrv, double* heaps, double* __restrict__ start,
-                              double* __restrict__ finish, double* chunk_last, double* last_out,
-                              uint32_t* refixed) {
-  if (threadIdx.x != 0) return;
+// The chunks in order (one block): a chunk whose check fails is staged in
+// shared memory and re-dispatched by one thread from the true incoming
+// state (its heap in shared memory up to KWP_HEAP servers).
+constexpr uint32_t KWP_HEAP = 2048;
+__global__ void __launch_bounds__(256) kw_fix_kernel(const double* __restrict__ R, const double* __restrict__ S,
+                                                     const uint32_t* nbp, uint32_t nsrv, double* heaps,
+                                                     double* __restrict__ start, double* __restrict__ finish,
+                                                     double* chunk_last, double* last_out, uint32_t* refixed) {
+  __shared__ double sR[KWP_CH], sS[KWP_CH];  // (R, S) in, (start, finish) out in place
+  __shared__ double sheap[KWP_HEAP];
+  __shared__ int s_fix;
   const uint32_t nb = *nbp, G = (nb + KWP_CH - 1) / KWP_CH;
-  double last = G ? chunk_last[0] : 0.0, in_max = last;  // (the state's max free time)
+  double last = G ? chunk_last[0] : 0.0, in_max = last;  // (the state's largest free time)
   uint32_t fixed = 0;
   for (uint32_t g = 1; g < G; ++g) {
-    const uint32_t lo = g * KWP_CH;
-    if (!(in_max <= R[lo])) {  // a server still busy at the chunk's first formation
-      double* heap = heaps + (size_t)g * nsrv;
+    const uint32_t lo = g * KWP_CH, m = min(KWP_CH, nb - lo);
+    if (threadIdx.x == 0) s_fix = !(in_max <= R[lo]);  // a server busy at the first formation
+    __syncthreads();
+    if (s_fix) {
+      double* heap = nsrv <= KWP_HEAP ? sheap : heaps + (size_t)g * nsrv;
       const double* prev = heaps + (size_t)(g - 1) * nsrv;
-      for (uint32_t q = 0; q < nsrv; ++q) heap[q] = prev[q];  // the true incoming state
-      double cl = 0.0;
-      kw_run(R, S, lo, min(nb, lo + KWP_CH), heap, nsrv, start, finish, cl);
-      chunk_last[g] = cl;
-      ++fixed;
+      for (uint32_t q = threadIdx.x; q < nsrv; q += blockDim.x) heap[q] = prev[q];  // the true state
+      for (uint32_t j = threadIdx.x; j < m; j += blockDim.x) {
+        sR[j] = R[lo + j];
+        sS[j] = S[lo + j];
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double cl = 0.0;
+        kw_run(sR, sS, 0, m, heap, nsrv, sR, sS, cl);
+        chunk_last[g] = cl;
+        ++fixed;
+      }
+      __syncthreads();
+      for (uint32_t j = threadIdx.x; j < m; j += blockDim.x) {
+        start[lo + j] = sR[j];
+        finish[lo + j] = sS[j];
+      }
+      if (nsrv <= KWP_HEAP)  // the chunk's outgoing state, for the next chunk
+        for (uint32_t q = threadIdx.x; q < nsrv; q += blockDim.x) heaps[(size_t)g * nsrv + q] = sheap[q];
+      __syncthreads();
     }
-    // the outgoing state's max: the largest free time (>= the previous max)
     in_max = fmax(in_max, chunk_last[g]);
     last = fmax(last, chunk_last[g]);
   }
-  *last_out = last;
-  *refixed = fixed;
+  if (threadIdx.x == 0) {
+    *last_out = last;
+    *refixed = fixed;
+  }
 }
 
 // ------------------------------------------------------------- requests
@@ -2562,8 +2586,8 @@ void trace_run(const TraceArgs& A, TraceResult* R, cudaStream_t s) {
       BB_CK(pool.alloc((void**)&refixed, 4));
       kw_spec_kernel<<<grid_for(G, 128), 128, 0, s>>>(dR, dS, nbp, A.n_servers, heaps, start, finish,
                                                       chunk_last);
-      kw_fix_kernel<<<1, 32, 0, s>>>(dR, dS, nbp, A.n_servers, heaps, start, finish, chunk_last, last_dev,
-                                     refixed);
+      kw_fix_kernel<<<1, 256, 0, s>>>(dR, dS, nbp, A.n_servers, heaps, start, finish, chunk_last, last_dev,
+                                      refixed);
       note_launch(2);
       BB_CK(cudaGetLastError());
       // busy time: the sequential sum of the services in dispatch order, exactly
