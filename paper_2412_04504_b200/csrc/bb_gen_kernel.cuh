@@ -478,12 +478,18 @@ __global__ void __launch_bounds__(kGenThreads, Q ? 2 : BB_GEN_MINB) gen_kernel(c
                 *reinterpret_cast<double2*>(q.A + o + u) = make_double2(at[u], at[u + 1]);
               // ids: a lane's eight consecutive ids are one 32 B sector; store
               // them together (half-sector stores cost several times more)
-              static_assert(U == 4, "ids are held for one iteration");
-              if ((i & 4u) == 0) {
-                idh = make_uint4(qid[0], qid[1], qid[2], qid[3]);
+              static_assert(U == 4 || U % 8 == 0, "ids go out a full 32 B sector at a time");
+              if constexpr (U == 4) {  // held for one iteration
+                if ((i & 4u) == 0) {
+                  idh = make_uint4(qid[0], qid[1], qid[2], qid[3]);
+                } else {
+                  *reinterpret_cast<uint4*>(q.Id + o - 4) = idh;
+                  *reinterpret_cast<uint4*>(q.Id + o) = make_uint4(qid[0], qid[1], qid[2], qid[3]);
+                }
               } else {
-                *reinterpret_cast<uint4*>(q.Id + o - 4) = idh;
-                *reinterpret_cast<uint4*>(q.Id + o) = make_uint4(qid[0], qid[1], qid[2], qid[3]);
+#pragma unroll
+                for (int u = 0; u < U; u += 4)
+                  *reinterpret_cast<uint4*>(q.Id + o + u) = make_uint4(qid[u], qid[u + 1], qid[u + 2], qid[u + 3]);
               }
             }
             if (PIPE) {
@@ -497,7 +503,7 @@ __global__ void __launch_bounds__(kGenThreads, Q ? 2 : BB_GEN_MINB) gen_kernel(c
         };
         if (bkt_ok) main_loop(std::true_type{});
         else main_loop(std::false_type{});
-        if (Q && (i & 4u)) *reinterpret_cast<uint4*>(q.Id + qlog_index(i - 4)) = idh;
+        if (Q && U == 4 && (i & 4u)) *reinterpret_cast<uint4*>(q.Id + qlog_index(i - 4)) = idh;
         // tail: fewer than U requests left, one at a time
         for (; !failed && i < n; ++i) {
           const Draw d0 = draw<SVC>(cyc_rank, nt, i, c2, c3, cyc);
