@@ -372,6 +372,11 @@ void bb_transfer_bytes(uint64_t* h2d_bytes, uint64_t* d2h_bytes, int reset);
 /* Device time (ms, CUDA events on the launch stream) of the last dominant
  * kernel launched by this thread and the launch count it covered. */
 double bb_last_kernel_ms(const char** name);
+/* Trace-mode CUDA graph accounting (cumulative; reset clears): runs captured
+ * into a graph and runs replayed from one.  The sync-free trace pipeline
+ * (no max_batch_wait, no detail batch copies) is captured on the second
+ * identical call and replayed from the third. */
+void bb_trace_graph_stats(uint64_t* captures, uint64_t* replays, int reset);
 
 #ifdef __cplusplus
 }

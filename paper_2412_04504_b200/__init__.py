@@ -764,6 +764,13 @@ def transfer_bytes(reset: bool = False):
     return h.value, d.value
 
 
+def trace_graph_stats(reset: bool = False):
+    """(captures, replays) of the trace pipeline's CUDA graph (cumulative)."""
+    c, r = C.c_uint64(), C.c_uint64()
+    _lib.bb_trace_graph_stats(C.byref(c), C.byref(r), int(reset))
+    return c.value, r.value
+
+
 def last_kernel_ms():
     name = C.c_char_p()
     ms = _lib.bb_last_kernel_ms(C.byref(name))

@@ -118,6 +118,7 @@ EXPORTS = [
     "bb_min_bins_for_throughput", "bb_expected_latency", "bb_exponential_service_bound",
     "bb_harmonic_number", "bb_assign_bin", "bb_brute_force_boundaries",
     "bb_points_shard_local_device", "bb_points_reduce_gathered_device", "bb_set_devices",
+    "bb_trace_graph_stats",
 ]
 
 
@@ -177,6 +178,8 @@ def load():
     lib.bb_launch_count.argtypes = [C.c_int]
     lib.bb_last_kernel_ms.restype = C.c_double
     lib.bb_last_kernel_ms.argtypes = [P(C.c_char_p)]
+    lib.bb_trace_graph_stats.restype = None
+    lib.bb_trace_graph_stats.argtypes = [P(C.c_uint64), P(C.c_uint64), C.c_int]
     lib.bb_template_edges.argtypes = [P(RunTemplateC), _dp, C.c_uint64, P(C.c_uint64)]
     lib.bb_service_of_keys.argtypes = [P(RunTemplateC), P(C.c_uint64), C.c_uint64, _dp]
     for f in ("bb_expected_service_time", "bb_throughput"):

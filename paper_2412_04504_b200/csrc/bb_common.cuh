@@ -15,6 +15,8 @@ namespace bb {
 
 // host-side launch accounting (bb_launch_count)
 void note_launch(unsigned n = 1);
+// kernels this thread has noted so far (a captured graph's launch count)
+unsigned long long launches_noted_here();
 
 // ----------------------------------------------------------------- Philox
 // Philox4x32-10 (Salmon et al., SC'11).  Replaces the reference's sequential

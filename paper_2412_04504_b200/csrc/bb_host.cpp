@@ -28,7 +28,12 @@ static std::atomic<unsigned long long> g_h2d{0}, g_d2h{0};
 // generated mode: exact per-replication p50/p99 (the reference always computes
 // them, simulator.hpp:289-301); off only for A/B measurements
 static std::atomic<int> g_gen_quantiles{1};
-void note_launch(unsigned n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+static thread_local unsigned long long t_launches = 0;
+void note_launch(unsigned n) {
+  g_launches.fetch_add(n, std::memory_order_relaxed);
+  t_launches += n;
+}
+unsigned long long launches_noted_here() { return t_launches; }
 }  // namespace bb
 
 namespace {
@@ -1664,6 +1669,10 @@ int bb_set_generated_quantiles(int on) { return bb::g_gen_quantiles.exchange(on 
 
 uint64_t bb_launch_count(int reset) {
   return reset ? bb::g_launches.exchange(0) : bb::g_launches.load();
+}
+
+void bb_trace_graph_stats(uint64_t* captures, uint64_t* replays, int reset) {
+  bb::trace_graph_stats(captures, replays, reset != 0);
 }
 
 double bb_last_kernel_ms(const char** name) {

@@ -46,5 +46,7 @@ struct TraceResult {
 
 // Runs the pipeline on `stream`; synchronises on it (metrics are read back).
 void trace_run(const TraceArgs& A, TraceResult* R, cudaStream_t stream);
+// runs captured into / replayed from the pipeline's CUDA graph
+void trace_graph_stats(uint64_t* captures, uint64_t* replays, bool reset);
 
 }  // namespace bb

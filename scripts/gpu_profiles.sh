@@ -6,6 +6,7 @@ timeout 900 python bench.py --impl reference > gpurun_out/r02_bench_reference.lo
 grep '^{' gpurun_out/r02_bench_reference.log | tail -1 > gpurun_out/r02_bench_reference.json
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/r02_bench_launches.csv python bench.py --reps 256 --steps 2 --warmup 1 --no-cpu-baseline > /dev/null 2>&1; echo "launches rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:gen_kernel -c 1 -o gpurun_out/r02_genq_full python bench.py --reps 2000 --steps 1 --warmup 0 --no-cpu-baseline --no-trace --no-ab --no-c5 > /dev/null 2>&1; echo "genq rc=$?"
+BB_WARP_MODE=1 timeout 900 ncu --set full --clock-control none --import-source on -k regex:genw_kernel -c 1 -o gpurun_out/r02_genw_full python scripts/warp_probe.py > /dev/null 2>&1; echo "genw rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"count_kernel|tscan_kernel|place_kernel|request_kernel|lindley_scan|binade_scan|binade_chain|sel_hist_kernel|sel_collect" -c 12 -o gpurun_out/r02_trace_full python scripts/trace_c2_once.py 1 > /dev/null 2>&1; echo "trace rc=$?"
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r02_trace_launches.csv python scripts/trace_c2_once.py 1 > /dev/null 2>&1; echo "trace launches rc=$?"
 ls -la gpurun_out | tail -12

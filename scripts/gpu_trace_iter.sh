@@ -1,5 +1,5 @@
 # trace-mode iteration: exactness tests, the C2 timing, a launch list and a full capture of the C2 kernels
-timeout 900 python -m pytest tests/test_gpu_trace.py tests/test_gpu_reference_rng.py -x -q -p no:cacheprovider > gpurun_out/r02_trace_tests.log 2>&1; echo "tests exit $?" >> gpurun_out/r02_trace_tests.log
+timeout 900 python -m pytest tests/test_gpu_trace_graph.py tests/test_gpu_trace.py tests/test_gpu_reference_rng.py -x -q -p no:cacheprovider > gpurun_out/r02_trace_tests.log 2>&1; echo "tests exit $?" >> gpurun_out/r02_trace_tests.log
 tail -3 gpurun_out/r02_trace_tests.log
 timeout 600 python scripts/trace_bench.py > gpurun_out/r02_trace_bench.log 2>&1; echo "trace bench exit $?"
 tail -c 1200 gpurun_out/r02_trace_bench.log
