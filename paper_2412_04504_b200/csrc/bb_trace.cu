@@ -309,14 +309,6 @@ __global__ void __launch_bounds__(TS_T) tscan_kernel(WS ws, uint32_t ntiles, uin
   if (tid == 0) ws.fin_cnt[b] = s_carry;
 }
 
-// batch-maximum slots: floor(total / B) full + 1 open batch per bin
-__global__ void sbase_kernel(WS ws, uint32_t k, uint32_t B) {
-  uint32_t acc = 0;
-  for (uint32_t q = 0; q < k; ++q) {
-    ws.info->sbase[q] = acc;
-    acc += (uint32_t)ws.fin_cnt[q] / B + 1;
-  }
-}
 
 template <bool TBOUT>  // true bins requested with given predictions (detail output)
 __global__ void __launch_bounds__(PT, 3) place_kernel(PartArgs P) {
@@ -329,7 +321,6 @@ __global__ void __launch_bounds__(PT, 3) place_kernel(PartArgs P) {
 
   const uint32_t tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const uint32_t k = P.k, n = P.n, B = P.B, t = blockIdx.x;
-  const Info* I = P.ws.info;
   for (uint32_t i = tid; i <= k; i += PT) s_edges[i] = P.edges[i];
   if (w == 0) {
     uint32_t jlo = 0, nfrag = 0;
@@ -341,15 +332,21 @@ __global__ void __launch_bounds__(PT, 3) place_kernel(PartArgs P) {
       nfrag = nxt > excl ? P.divB.div(nxt - 1) - jlo + 1 : 0;  // batches this tile touches
       s_excl[lane] = excl;
       s_jlo[lane] = jlo;
-      s_sbase[lane] = I->sbase[lane];
     }
-    uint32_t incl = nfrag;
+    // batch-maximum slots: floor(total / B) full + 1 open batch per bin
+    const uint32_t nslot = lane < k ? P.divB.div((uint32_t)P.ws.fin_cnt[lane]) + 1 : 0u;
+    uint32_t incl = nfrag, sincl = nslot;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= (uint32_t)o) incl += v;
+      const uint32_t sv = __shfl_up_sync(0xffffffffu, sincl, o);
+      if (lane >= (uint32_t)o) incl += v, sincl += sv;
     }
-    if (lane < k) s_fbase[lane] = incl - nfrag;
+    if (lane < k) {
+      s_fbase[lane] = incl - nfrag;
+      s_sbase[lane] = sincl - nslot;
+      if (t == 0) P.ws.info->sbase[lane] = sincl - nslot;  // for the kernels after this one
+    }
     if (lane == 31) s_nfrag_total = incl;
     uint32_t cb = lane < k ? jlo : 0;  // closings before this tile = sum_b floor(excl_b / B)
 #pragma unroll
@@ -2370,10 +2367,9 @@ static void trace_run_impl(const TraceArgs& A, TraceResult* R, cudaStream_t s, T
     }
     count_kernel<<<ntiles, PT, 0, s>>>(P);
     tscan_kernel<<<k, TS_T, 0, s>>>(ws, ntiles, k, B);
-    sbase_kernel<<<1, 1, 0, s>>>(ws, k, B);
     if (P.pred && P.tb_out) place_kernel<true><<<ntiles, PT, 0, s>>>(P);
     else place_kernel<false><<<ntiles, PT, 0, s>>>(P);
-    note_launch(4);
+    note_launch(3);
     BB_CK(cudaGetLastError());
   }
   BB_CK(record(ev1));

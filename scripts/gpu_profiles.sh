@@ -9,5 +9,13 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:gen_
 BB_WARP_MODE=1 timeout 900 ncu --set full --clock-control none --import-source on -k regex:genw_kernel -c 1 -o gpurun_out/r02_genw_full python scripts/warp_probe.py > /dev/null 2>&1; echo "genw rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"count_kernel|tscan_kernel|place_kernel|request_kernel|lindley_scan|binade_scan|binade_chain|sel_hist_kernel|sel_collect" -c 12 -o gpurun_out/r02_trace_full python scripts/trace_c2_once.py 1 > /dev/null 2>&1; echo "trace rc=$?"
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r02_trace_launches.csv python scripts/trace_c2_once.py 1 > /dev/null 2>&1; echo "trace launches rc=$?"
-ls -la gpurun_out | tail -12
+# summaries on the box (the .ncu-rep files exceed gpurun's 64 MiB copy-back)
+python scripts/ncu_summary.py launches gpurun_out/r02_bench_launches.csv gpurun_out/r02_bench_launches.md > /dev/null
+python scripts/ncu_summary.py launches gpurun_out/r02_trace_launches.csv gpurun_out/r02_trace_c2_launches.md > /dev/null
+python scripts/ncu_summary.py full gpurun_out/r02_genq_full.ncu-rep gpurun_out/r02_gen_kernel_q_ncu.json 2.1e10
+python scripts/ncu_lines.py gpurun_out/r02_genq_full.ncu-rep 2.1e10 > gpurun_out/r02_gen_kernel_q_lines.txt
+python scripts/ncu_summary.py full gpurun_out/r02_genw_full.ncu-rep gpurun_out/r02_genw_kernel_ncu.json 4.736e9
+python scripts/ncu_summary.py full gpurun_out/r02_trace_full.ncu-rep gpurun_out/r02_trace_c2_ncu.json 1e7
+rm -f gpurun_out/*.ncu-rep
+ls -la gpurun_out | tail -16
 cat gpurun_out/r02_bench_default.json | cut -c1-1500
