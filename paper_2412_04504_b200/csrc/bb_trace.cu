@@ -161,101 +161,124 @@ __device__ __forceinline__ uint32_t part_bin(const PartArgs& P, const double* ed
 
 // Counting needs no order: thread t takes the PIPT consecutive requests at
 // tile + t * PIPT, loaded as one 8-byte vector of predictions (or 16-byte
-// vectors of services and error uniforms) when aligned.
+// vectors of services and error uniforms) when aligned.  Blocks stride over
+// the tiles (a few per block, the next tile's predictions loaded while the
+// current one is counted): per-tile work is small, so block launches and
+// load latency, not bytes, would bound a block per tile.
+__device__ __forceinline__ uint2 count_load_pred(const PartArgs& P, uint32_t tile, uint32_t tid) {
+  const uint64_t i0 = (uint64_t)tile * PTILE + (uint64_t)tid * PIPT;
+  if (i0 + PIPT <= P.n && P.vec_ok) return *reinterpret_cast<const uint2*>(P.pred + i0);
+  uint2 v = make_uint2(0, 0);
+#pragma unroll
+  for (int j = 0; j < PIPT; ++j)
+    if (i0 + j < P.n) (j < 4 ? v.x : v.y) |= (uint32_t)P.pred[i0 + j] << (8 * (j & 3));
+  return v;
+}
+
+template <int NG>  // 4-bit count groups of 8 bins: ceil(k / 8)
 __global__ void __launch_bounds__(PT) count_kernel(PartArgs P) {
   __shared__ double s_edges[BB_TRACE_MAX_BINS + 1];
   __shared__ uint32_t s_cnt[PNW][32];
   static_assert(PIPT == 8, "one 8-byte vector of predictions per thread");
   const uint32_t tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const uint32_t k = P.k, n = P.n;
+  uint2 nxt = make_uint2(0, 0);
+  if (P.pred && blockIdx.x < P.ntiles) nxt = count_load_pred(P, blockIdx.x, tid);
   for (uint32_t i = tid; i <= k; i += PT) s_edges[i] = P.edges[i];
   __syncthreads();
-  const uint64_t i0 = (uint64_t)blockIdx.x * PTILE + (uint64_t)tid * PIPT;
-  const bool full = i0 + PIPT <= n && P.vec_ok;
-  uint32_t b[PIPT];
-  if (P.pred) {
-    if (full) {
-      const uint2 v = *reinterpret_cast<const uint2*>(P.pred + i0);
+  for (uint32_t tile = blockIdx.x; tile < P.ntiles; tile += gridDim.x) {
+    const uint64_t i0 = (uint64_t)tile * PTILE + (uint64_t)tid * PIPT;
+    const bool full = i0 + PIPT <= n && P.vec_ok;
+    uint32_t b[PIPT];
+    if (P.pred) {
+      const uint2 v = nxt;
+      if (tile + gridDim.x < P.ntiles) nxt = count_load_pred(P, tile + gridDim.x, tid);
 #pragma unroll
       for (int j = 0; j < PIPT; ++j) b[j] = ((j < 4 ? v.x : v.y) >> (8 * (j & 3))) & 0xFF;
-    } else {
+      // every byte in [1, k]? (four at a time; the per-request check only on a miss or the tail)
+      const uint32_t kk = k * 0x01010101u;
+      const bool ok = i0 + PIPT <= n && !(__vcmpeq4(v.x, 0u) | __vcmpeq4(v.y, 0u) |
+                                          __vcmpgtu4(v.x, kk) | __vcmpgtu4(v.y, kk));
+      if (!ok) {
 #pragma unroll
-      for (int j = 0; j < PIPT; ++j) b[j] = i0 + j < n ? P.pred[i0 + j] : 0u;
-    }
-#pragma unroll
-    for (int j = 0; j < PIPT; ++j)
-      if (i0 + j < n && (b[j] < 1 || b[j] > k)) {
-        raise_error(P.ws.err, i0 + j, BB_EINVAL, (double)b[j], 3);
-        b[j] = 0;
-      }
-  } else {
-    double sv[PIPT];
-    if (full) {
-#pragma unroll
-      for (int j = 0; j < PIPT; j += 2) {
-        const double2 x = *reinterpret_cast<const double2*>(P.s + i0 + j);
-        sv[j] = x.x;
-        sv[j + 1] = x.y;
+        for (int j = 0; j < PIPT; ++j)
+          if (i0 + j < n && (b[j] < 1 || b[j] > k)) {
+            raise_error(P.ws.err, i0 + j, BB_EINVAL, (double)b[j], 3);
+            b[j] = 0;
+          }
       }
     } else {
+      double sv[PIPT];
+      if (full) {
 #pragma unroll
-      for (int j = 0; j < PIPT; ++j) sv[j] = i0 + j < n ? P.s[i0 + j] : 0.0;
-    }
-    uint32_t tbs[PIPT];
+        for (int j = 0; j < PIPT; j += 2) {
+          const double2 x = *reinterpret_cast<const double2*>(P.s + i0 + j);
+          sv[j] = x.x;
+          sv[j + 1] = x.y;
+        }
+      } else {
 #pragma unroll
-    for (int j = 0; j < PIPT; ++j) {
-      b[j] = tbs[j] = 0;
-      if (i0 + j < n) b[j] = part_bin(P, s_edges, i0 + j, sv[j], tbs[j]);
-    }
-    if (full) {  // predicted (and true) bins, one vector store each
-      uint2 pv = make_uint2(0, 0), tv = make_uint2(0, 0);
+        for (int j = 0; j < PIPT; ++j) sv[j] = i0 + j < n ? P.s[i0 + j] : 0.0;
+      }
+      uint32_t tbs[PIPT];
 #pragma unroll
       for (int j = 0; j < PIPT; ++j) {
-        (j < 4 ? pv.x : pv.y) |= b[j] << (8 * (j & 3));
-        (j < 4 ? tv.x : tv.y) |= tbs[j] << (8 * (j & 3));
+        b[j] = tbs[j] = 0;
+        if (i0 + j < n) b[j] = part_bin(P, s_edges, i0 + j, sv[j], tbs[j]);
       }
-      *reinterpret_cast<uint2*>(P.ws.pb8 + i0) = pv;
-      if (P.tb_out) *reinterpret_cast<uint2*>(P.tb_out + i0) = tv;
-    } else {
+      if (full) {  // predicted (and true) bins, one vector store each
+        uint2 pv = make_uint2(0, 0), tv = make_uint2(0, 0);
 #pragma unroll
-      for (int j = 0; j < PIPT; ++j)
-        if (i0 + j < n) {
-          P.ws.pb8[i0 + j] = (uint8_t)b[j];
-          if (P.tb_out) P.tb_out[i0 + j] = (uint8_t)tbs[j];
+        for (int j = 0; j < PIPT; ++j) {
+          (j < 4 ? pv.x : pv.y) |= b[j] << (8 * (j & 3));
+          (j < 4 ? tv.x : tv.y) |= tbs[j] << (8 * (j & 3));
         }
+        *reinterpret_cast<uint2*>(P.ws.pb8 + i0) = pv;
+        if (P.tb_out) *reinterpret_cast<uint2*>(P.tb_out + i0) = tv;
+      } else {
+#pragma unroll
+        for (int j = 0; j < PIPT; ++j)
+          if (i0 + j < n) {
+            P.ws.pb8[i0 + j] = (uint8_t)b[j];
+            if (P.tb_out) P.tb_out[i0 + j] = (uint8_t)tbs[j];
+          }
+      }
     }
-  }
-  // per-thread counts in 4-bit fields (bin q+1 at nib[q / 8], bits 4 (q % 8);
-  // at most PIPT = 8 per thread), then spread to 16-bit fields and summed over
-  // the warp with one integer reduction per four bins (<= 256 per field)
-  uint32_t nib[4] = {0u, 0u, 0u, 0u};
+    // per-thread counts in 4-bit fields (bin q+1 at nib[q / 8], bits 4 (q % 8);
+    // at most PIPT = 8 per thread), then spread to 16-bit fields and summed over
+    // the warp with one integer reduction per four bins (<= 256 per field)
+    uint32_t nib[NG] = {};
 #pragma unroll
-  for (int j = 0; j < PIPT; ++j) {
-    const uint32_t q = b[j] - 1, inc = b[j] ? 1u << (4 * (q & 7)) : 0u;
+    for (int j = 0; j < PIPT; ++j) {
+      if (NG == 1) {  // b in [0, 8] (0: invalid, not counted)
+        nib[0] += b[j] ? 1u << (4 * b[j] - 4) : 0u;
+      } else {
+        const uint32_t q = b[j] - 1, inc = b[j] ? 1u << (4 * (q & 7)) : 0u;
 #pragma unroll
-    for (int g = 0; g < 4; ++g) nib[g] += (q >> 3) == (uint32_t)g ? inc : 0u;
-  }
-  const uint32_t ng = (k + 7) / 8;
-#pragma unroll
-  for (int g = 0; g < 4; ++g) {
-    if ((uint32_t)g >= ng) break;
-    const uint32_t ev = nib[g] & 0x0F0F0F0Fu, od = (nib[g] >> 4) & 0x0F0F0F0Fu;
-    const uint32_t r0 = __reduce_add_sync(0xffffffffu, ev & 0x00FF00FFu);         // bins 8g+1, +5
-    const uint32_t r1 = __reduce_add_sync(0xffffffffu, (ev >> 8) & 0x00FF00FFu);  // bins 8g+3, +7
-    const uint32_t r2 = __reduce_add_sync(0xffffffffu, od & 0x00FF00FFu);         // bins 8g+2, +6
-    const uint32_t r3 = __reduce_add_sync(0xffffffffu, (od >> 8) & 0x00FF00FFu);  // bins 8g+4, +8
-    if (lane == 0) {
-      const uint32_t c[8] = {r0 & 0xFFFF, r2 & 0xFFFF, r1 & 0xFFFF, r3 & 0xFFFF,
-                             r0 >> 16, r2 >> 16, r1 >> 16, r3 >> 16};
-#pragma unroll
-      for (int q = 0; q < 8; ++q) s_cnt[w][8 * g + q] = c[q];
+        for (int g = 0; g < NG; ++g) nib[g] += (q >> 3) == (uint32_t)g ? inc : 0u;
+      }
     }
-  }
-  __syncthreads();
-  if (w == 0 && lane < k) {
-    uint32_t c = 0;
-    for (int w2 = 0; w2 < PNW; ++w2) c += s_cnt[w2][lane];
-    P.ws.tcount[(uint64_t)lane * P.ntiles + blockIdx.x] = c;  // bin-major: a bin's tiles contiguous
+#pragma unroll
+    for (int g = 0; g < NG; ++g) {
+      const uint32_t ev = nib[g] & 0x0F0F0F0Fu, od = (nib[g] >> 4) & 0x0F0F0F0Fu;
+      const uint32_t r0 = __reduce_add_sync(0xffffffffu, ev & 0x00FF00FFu);         // bins 8g+1, +5
+      const uint32_t r1 = __reduce_add_sync(0xffffffffu, (ev >> 8) & 0x00FF00FFu);  // bins 8g+3, +7
+      const uint32_t r2 = __reduce_add_sync(0xffffffffu, od & 0x00FF00FFu);         // bins 8g+2, +6
+      const uint32_t r3 = __reduce_add_sync(0xffffffffu, (od >> 8) & 0x00FF00FFu);  // bins 8g+4, +8
+      if (lane == 0) {
+        const uint32_t c[8] = {r0 & 0xFFFF, r2 & 0xFFFF, r1 & 0xFFFF, r3 & 0xFFFF,
+                               r0 >> 16, r2 >> 16, r1 >> 16, r3 >> 16};
+#pragma unroll
+        for (int q = 0; q < 8; ++q) s_cnt[w][8 * g + q] = c[q];
+      }
+    }
+    __syncthreads();
+    if (w == 0 && lane < k) {
+      uint32_t c = 0;
+      for (int w2 = 0; w2 < PNW; ++w2) c += s_cnt[w2][lane];
+      P.ws.tcount[(uint64_t)lane * P.ntiles + tile] = c;  // bin-major: a bin's tiles contiguous
+    }
+    __syncthreads();  // s_cnt is rewritten by the next tile
   }
 }
 
@@ -310,56 +333,24 @@ __global__ void __launch_bounds__(TS_T) tscan_kernel(WS ws, uint32_t ntiles, uin
 }
 
 
+// Three barriers per tile: warp 0 lays out the tile's per-bin bases while
+// every warp ranks its own requests (no barrier before that); each warp then
+// adds the earlier warps' counts itself.
 template <bool TBOUT>  // true bins requested with given predictions (detail output)
 __global__ void __launch_bounds__(PT, 3) place_kernel(PartArgs P) {
-  __shared__ double s_edges[BB_TRACE_MAX_BINS + 1];
-  __shared__ uint32_t s_run[PNW][32], s_woff[PNW][32];
-  __shared__ uint32_t s_excl[32], s_sbase[32], s_jlo[32], s_fbase[32];
+  __shared__ uint32_t s_run[PNW][32];   // per warp: its requests per bin
+  __shared__ uint32_t s_base[PNW][32];  // per warp: its rank base per bin
+  __shared__ uint32_t s_excl[32];       // tile prefix per bin
+  __shared__ uint32_t s_fr0[32];        // fragment index of the bin's batch 0 (fbase - jlo)
+  __shared__ uint32_t s_soff[32];       // smax slot of fragment f of the bin: f + soff
   __shared__ uint32_t s_shi[PTILE + 32], s_slo[PTILE + 32];  // fragment maxima: high, low words
-  __shared__ uint32_t s_wclose[PNW];
-  __shared__ uint32_t s_closebase, s_flags, s_nfrag_total;
+  __shared__ uint8_t s_fbin[PTILE + 32];                     // the bin of each fragment
+  __shared__ uint32_t s_wclose[PNW], s_wflags[PNW];
+  __shared__ uint32_t s_closebase, s_nfrag_total;
 
   const uint32_t tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const uint32_t k = P.k, n = P.n, B = P.B, t = blockIdx.x;
-  for (uint32_t i = tid; i <= k; i += PT) s_edges[i] = P.edges[i];
-  if (w == 0) {
-    uint32_t jlo = 0, nfrag = 0;
-    if (lane < k) {
-      const uint32_t excl = P.ws.tcount[(uint64_t)lane * P.ntiles + t];
-      const uint32_t nxt = t + 1 < P.ntiles ? P.ws.tcount[(uint64_t)lane * P.ntiles + t + 1]
-                                            : (uint32_t)P.ws.fin_cnt[lane];
-      jlo = P.divB.div(excl);
-      nfrag = nxt > excl ? P.divB.div(nxt - 1) - jlo + 1 : 0;  // batches this tile touches
-      s_excl[lane] = excl;
-      s_jlo[lane] = jlo;
-    }
-    // batch-maximum slots: floor(total / B) full + 1 open batch per bin
-    const uint32_t nslot = lane < k ? P.divB.div((uint32_t)P.ws.fin_cnt[lane]) + 1 : 0u;
-    uint32_t incl = nfrag, sincl = nslot;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
-      const uint32_t sv = __shfl_up_sync(0xffffffffu, sincl, o);
-      if (lane >= (uint32_t)o) incl += v, sincl += sv;
-    }
-    if (lane < k) {
-      s_fbase[lane] = incl - nfrag;
-      s_sbase[lane] = sincl - nslot;
-      if (t == 0) P.ws.info->sbase[lane] = sincl - nslot;  // for the kernels after this one
-    }
-    if (lane == 31) s_nfrag_total = incl;
-    uint32_t cb = lane < k ? jlo : 0;  // closings before this tile = sum_b floor(excl_b / B)
-#pragma unroll
-    for (int o = 16; o; o >>= 1) cb += __shfl_xor_sync(0xffffffffu, cb, o);
-    if (lane == 0) {
-      s_closebase = cb;
-      s_flags = 0;
-    }
-  }
-  s_run[w][lane] = 0;
-  __syncthreads();
-  for (uint32_t i = tid; i < s_nfrag_total; i += PT) s_shi[i] = s_slo[i] = 0u;
-
+  // the tile's requests first: their loads are in flight across the prologue
   const uint64_t wbase = (uint64_t)t * PTILE + w * (32 * PIPT);
   const double a0 = P.a[0];
   const uint8_t* pbsrc = P.pred ? P.pred : P.ws.pb8;
@@ -372,11 +363,60 @@ __global__ void __launch_bounds__(PT, 3) place_kernel(PartArgs P) {
     av[j] = v ? P.a[idx] : 0.0;
     sv[j] = v ? P.s[idx] : 0.0;
     pr[j] = v ? pbsrc[idx] : 0u;
-    if (pr[j] > k) pr[j] = 0;  // an invalid given prediction (count_kernel reported it)
   }
+  s_run[w][lane] = 0;
+  if (w == 0) {  // the tile's per-bin bases (read after the first barrier)
+    uint32_t jlo = 0, nfrag = 0, excl = 0;
+    if (lane < k) {
+      excl = P.ws.tcount[(uint64_t)lane * P.ntiles + t];
+      const uint32_t nxt = t + 1 < P.ntiles ? P.ws.tcount[(uint64_t)lane * P.ntiles + t + 1]
+                                            : (uint32_t)P.ws.fin_cnt[lane];
+      jlo = P.divB.div(excl);
+      nfrag = nxt > excl ? P.divB.div(nxt - 1) - jlo + 1 : 0;  // batches this tile touches
+    }
+    // batch-maximum slots: floor(total / B) full + 1 open batch per bin
+    const uint32_t nslot = lane < k ? P.divB.div((uint32_t)P.ws.fin_cnt[lane]) + 1 : 0u;
+    uint32_t incl = nfrag, sincl = nslot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+      const uint32_t sv2 = __shfl_up_sync(0xffffffffu, sincl, o);
+      if (lane >= (uint32_t)o) incl += v, sincl += sv2;
+    }
+    const uint32_t fbase = incl - nfrag, sbase = sincl - nslot;
+    if (lane < k) {
+      s_excl[lane] = excl;
+      s_fr0[lane] = fbase - jlo;
+      s_soff[lane] = sbase + jlo - fbase;
+      if (t == 0) P.ws.info->sbase[lane] = sbase;  // for the kernels after this one
+      for (uint32_t x = 0; x < nfrag; ++x) s_fbin[fbase + x] = (uint8_t)lane;
+    }
+    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+    for (uint32_t i = lane; i < total; i += 32) s_shi[i] = s_slo[i] = 0u;
+    uint32_t cb = lane < k ? jlo : 0;  // closings before this tile = sum_b floor(excl_b / B)
+#pragma unroll
+    for (int o = 16; o; o >>= 1) cb += __shfl_xor_sync(0xffffffffu, cb, o);
+    if (lane == 0) {
+      s_closebase = cb;
+      s_nfrag_total = total;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < PIPT; ++j)
+    if (pr[j] > k) pr[j] = 0;  // an invalid given prediction (count_kernel reported it)
+  __syncwarp();
+
   uint32_t flags = 0, ties = 0;
   const uint32_t lt = lanemask_lt();
-  const double e_lo = s_edges[0], e_hi = s_edges[k];
+  // service support test on the IEEE bits: positive finite doubles order
+  // like their bit patterns, so lo <= x <= hi is one subtraction and one
+  // unsigned compare (negative, NaN and infinite services fall outside)
+  const double e_lo = P.edges[0], e_hi = P.edges[k];
+  const double lo_v = e_lo > 0 ? e_lo : 4.9406564584124654e-324;
+  const bool none = !(e_hi >= lo_v) || isnan(e_lo);
+  const unsigned long long lo_b = (unsigned long long)__double_as_longlong(lo_v);
+  const unsigned long long span =
+      none ? 0ull : (unsigned long long)__double_as_longlong(fmin(e_hi, 1.7976931348623157e308)) - lo_b;
   uint32_t pbk[PIPT / 4] = {};  // the bins, packed (the records need them after pr holds ranks)
 #pragma unroll
   for (int j = 0; j < PIPT; ++j) {
@@ -399,9 +439,9 @@ __global__ void __launch_bounds__(PT, 3) place_kernel(PartArgs P) {
         if (TBOUT) {
           uint32_t tb = 0;
           if (!(sj > 0) || !isfinite(sj)) raise_error(P.ws.err, idx, BB_EDOMAIN, sj, 1);
-          else if ((tb = assign_bin(s_edges, k, sj)) == 0) raise_error(P.ws.err, idx, BB_EDOMAIN, sj, 2);
+          else if ((tb = assign_bin(P.edges, k, sj)) == 0) raise_error(P.ws.err, idx, BB_EDOMAIN, sj, 2);
           P.tb_out[idx] = (uint8_t)tb;
-        } else if (!(sj > 0 && sj < CUDART_INF && sj >= e_lo && sj <= e_hi)) {
+        } else if (none || (unsigned long long)__double_as_longlong(sj) - lo_b > span) {
           raise_error(P.ws.err, idx, BB_EDOMAIN, sj, !(sj > 0) || !isfinite(sj) ? 1 : 2);
         }
       }
@@ -422,17 +462,21 @@ __global__ void __launch_bounds__(PT, 3) place_kernel(PartArgs P) {
       if (((ties >> j) & 1u) && idx >= B && P.a[idx - B] == av[j]) flags |= FL_TIE_GT_B;
     }
   }
-  if (flags) atomicOr(&s_flags, flags);
-  __syncthreads();
-  if (w == 0 && lane < k) {  // warp offsets within the tile
-    uint32_t acc = 0;
-    for (int w2 = 0; w2 < PNW; ++w2) {
-      s_woff[w2][lane] = acc;
-      acc += s_run[w2][lane];
-    }
+  flags = __reduce_or_sync(0xffffffffu, flags);
+  if (lane == 0) s_wflags[w] = flags;
+  __syncthreads();  // (1) per-warp counts, the tile's bases
+  if (lane < k) {  // this warp's rank base per bin: tile prefix + earlier warps
+    uint32_t acc = s_excl[lane];
+    for (uint32_t w2 = 0; w2 < w; ++w2) acc += s_run[w2][lane];
+    s_base[w][lane] = acc;
   }
-  if (tid == 0 && s_flags) atomicOr(P.ws.flags, s_flags);
-  __syncthreads();
+  if (tid == 0) {
+    uint32_t f = 0;
+#pragma unroll
+    for (int w2 = 0; w2 < PNW; ++w2) f |= s_wflags[w2];
+    if (f) atomicOr(P.ws.flags, f);
+  }
+  __syncwarp();
 
   // global rank, batch, fragment maximum (the IEEE bits of the positive
   // services order like their values: a max of the high words, then of the
@@ -447,12 +491,12 @@ __global__ void __launch_bounds__(PT, 3) place_kernel(PartArgs P) {
     fr[j] = ~0u;
     if (pb) {
       const uint32_t b = pb - 1;
-      const uint32_t rk = s_excl[b] + s_woff[w][b] + (pr[j] >> 8);
+      const uint32_t rk = s_base[w][b] + (pr[j] >> 8);
       const uint32_t jb = P.divB.div(rk);
-      fr[j] = s_fbase[b] + (jb - s_jlo[b]);
+      fr[j] = s_fr0[b] + jb;
       atomicMax(&s_shi[fr[j]], (uint32_t)__double2hiint(sv[j]));
       closing = rk - jb * B == B - 1;
-      pr[j] = rk;  // from here on: the rank (the bin stays in pbsrc)
+      pr[j] = jb;  // from here on: the batch (the bin stays in pbk)
       const uint64_t idx = wbase + j * 32 + lane;
       P.ws.rank[idx] = rk;
     }
@@ -460,19 +504,11 @@ __global__ void __launch_bounds__(PT, 3) place_kernel(PartArgs P) {
     wclose += __popc(__ballot_sync(0xffffffffu, closing));
   }
   if (lane == 0) s_wclose[w] = wclose;
-  __syncthreads();
+  __syncthreads();  // (2) high words final
 #pragma unroll
   for (int j = 0; j < PIPT; ++j)
     if (fr[j] != ~0u && s_shi[fr[j]] == (uint32_t)__double2hiint(sv[j]))
       atomicMax(&s_slo[fr[j]], (uint32_t)__double2loint(sv[j]));
-  __syncthreads();
-  // fragment maxima into the (bin, batch) slots: one global max per fragment
-  for (uint32_t f = tid; f < s_nfrag_total; f += PT) {
-    uint32_t b = 0;
-    while (b + 1 < k && s_fbase[b + 1] <= f) ++b;
-    atomicMax(P.ws.smax + s_sbase[b] + s_jlo[b] + (f - s_fbase[b]),
-              ((unsigned long long)s_shi[f] << 32) | s_slo[f]);
-  }
   // closing records, in closing-request order (dispatch order on the fast path)
   uint32_t run = s_closebase;
   for (uint32_t w2 = 0; w2 < w; ++w2) run += s_wclose[w2];
@@ -485,11 +521,15 @@ __global__ void __launch_bounds__(PT, 3) place_kernel(PartArgs P) {
       const uint32_t q = run + __popc(bal & lt);
       P.ws.recR[q] = av[j];
       P.ws.recBin[q] = (uint8_t)(pbk[j / 4] >> (8 * (j & 3)));
-      P.ws.recJ[q] = P.divB.div(pr[j]);
+      P.ws.recJ[q] = pr[j];
       P.ws.recC[q] = (uint32_t)idx;
     }
     run += __popc(bal);
   }
+  __syncthreads();  // (3) low words final
+  // fragment maxima into the (bin, batch) slots: one global max per fragment
+  for (uint32_t f = tid; f < s_nfrag_total; f += PT)
+    atomicMax(P.ws.smax + f + s_soff[s_fbin[f]], ((unsigned long long)s_shi[f] << 32) | s_slo[f]);
 }
 
 // the service of batch (bin b+1, j): max over its members (place_kernel)
@@ -1602,56 +1642,6 @@ __global__ void sel_hist_kernel(const unsigned long long* __restrict__ key, uint
     if (h[i]) atomicAdd(&hist[i], h[i]);
 }
 
-// prefix over the level-1 histogram; per target: bucket, residual rank, range
-__global__ void __launch_bounds__(1024) sel_find_kernel(SelState* S, const uint32_t* hist,
-                                                        uint32_t cap) {
-  __shared__ unsigned long long ps[HBINS];
-  const int t = threadIdx.x;
-  for (int i = t; i < HBINS; i += blockDim.x) ps[i] = hist[i];
-  __syncthreads();
-  for (int o = 1; o < HBINS; o <<= 1) {  // inclusive Hillis-Steele scan (4096 bins)
-    unsigned long long add[HBINS / 1024];
-    for (int q = 0; q < HBINS / 1024; ++q) {
-      const int i = t + q * 1024;
-      add[q] = i >= o ? ps[i - o] : 0ull;
-    }
-    __syncthreads();
-    for (int q = 0; q < HBINS / 1024; ++q) ps[t + q * 1024] += add[q];
-    __syncthreads();
-  }
-  if (t == 0) {
-    unsigned long long need = 0;
-    S->need_collect = 0;
-    for (uint32_t q = 0; q < S->nt; ++q) {
-      const unsigned long long r = S->rank[q];
-      int lo = 0, hi = HBINS - 1;  // first bucket with inclusive count > r
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (ps[mid] > r) hi = mid;
-        else lo = mid + 1;
-      }
-      const unsigned long long before = lo ? ps[lo - 1] : 0ull;
-      S->rank[q] = r - before;
-      S->bucket[q] = lo;
-      const unsigned long long blo = S->base + ((unsigned long long)lo << S->shift);
-      unsigned long long bhi = blo + ((1ull << S->shift) - 1);
-      if (bhi > S->top || bhi < blo) bhi = S->top;
-      S->lo[q] = blo;
-      S->hi[q] = bhi;
-      if (blo == bhi) {
-        S->result[q] = blo;
-      } else {
-        bool dup = false;
-        for (uint32_t z = 0; z < q; ++z) dup |= S->lo[z] == blo && S->hi[z] != S->lo[z];
-        if (!dup) need += ps[lo] - before;
-        S->need_collect = 1;
-      }
-    }
-    S->overflow = need > cap;
-  }
-}
-
-
 // Block-wide bucket search (blockDim == 1024): the bucket b of h[0..nb) with
 // prefix(b) <= r < prefix(b) + h[b]; writes *bucket and *before.
 __device__ __forceinline__ void block_find(const uint32_t* h, int nb, unsigned long long r,
@@ -1693,6 +1683,44 @@ __device__ __forceinline__ void block_find(const uint32_t* h, int nb, unsigned l
     }
   }
   __syncthreads();
+}
+
+// per target: bucket, residual rank, range (1024 threads; a block-wide
+// search per target over the level-1 histogram)
+__global__ void __launch_bounds__(1024) sel_find_kernel(SelState* S, const uint32_t* hist,
+                                                        uint32_t cap) {
+  __shared__ uint32_t h[HBINS];
+  __shared__ uint32_t s_b;
+  __shared__ unsigned long long s_before;
+  const int t = threadIdx.x;
+  for (int i = t; i < HBINS; i += blockDim.x) h[i] = hist[i];
+  __syncthreads();
+  unsigned long long need = 0;
+  if (t == 0) S->need_collect = 0;
+  const uint32_t nt = S->nt;
+  for (uint32_t q = 0; q < nt; ++q) {
+    block_find(h, HBINS, S->rank[q], &s_b, &s_before);
+    if (t == 0) {
+      const uint32_t b = s_b;
+      S->rank[q] -= s_before;
+      S->bucket[q] = b;
+      const unsigned long long blo = S->base + ((unsigned long long)b << S->shift);
+      unsigned long long bhi = blo + ((1ull << S->shift) - 1);
+      if (bhi > S->top || bhi < blo) bhi = S->top;
+      S->lo[q] = blo;
+      S->hi[q] = bhi;
+      if (blo == bhi) {
+        S->result[q] = blo;
+      } else {
+        bool dup = false;
+        for (uint32_t z = 0; z < q; ++z) dup |= S->lo[z] == blo && S->hi[z] != S->lo[z];
+        if (!dup) need += h[b];
+        S->need_collect = 1;
+      }
+    }
+    __syncthreads();
+  }
+  if (t == 0) S->overflow = need > cap;
 }
 
 // level 2 over the full key array: every unresolved target's bucket split
@@ -1785,12 +1813,35 @@ __global__ void sel_collect_kernel(const unsigned long long* __restrict__ key, u
 }
 
 // refine every unresolved target on the candidates, all levels in smem
+constexpr uint32_t kRefineDirect = 512;
 __global__ void __launch_bounds__(1024) sel_refine_kernel(SelState* S,
                                                           const unsigned long long* __restrict__ cand) {
   __shared__ uint32_t h[HBINS];
   __shared__ unsigned long long s_lo, s_hi, s_rank;
+  __shared__ unsigned long long s_c[kRefineDirect];
   if (!S->need_collect || S->overflow) return;
   const uint32_t m = S->ncand;
+  if (m <= kRefineDirect) {  // few candidates: rank each one directly (m^2 compares)
+    for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) s_c[i] = cand[i];
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
+      const unsigned long long v = s_c[i];
+      for (uint32_t q = 0; q < S->nt; ++q) {
+        const unsigned long long lo = S->lo[q], hi = S->hi[q];
+        if (lo == hi || v < lo || v > hi) continue;
+        uint32_t lt = 0, eq = 0;
+        for (uint32_t j = 0; j < m; ++j) {
+          const unsigned long long c = s_c[j];
+          const bool in = c >= lo && c <= hi;
+          lt += in && c < v;
+          eq += c == v;
+        }
+        const unsigned long long r = S->rank[q];
+        if (lt <= r && r < (unsigned long long)lt + eq) S->result[q] = v;  // (ties write the same value)
+      }
+    }
+    return;
+  }
   for (uint32_t q = 0; q < S->nt; ++q) {
     if (threadIdx.x == 0) {
       s_lo = S->lo[q];
@@ -2160,6 +2211,35 @@ struct Readback {
   SelState hs;
 };
 
+// Everything the host reads back, gathered on the device by one small
+// kernel: one copy (or, into the graph's pinned struct, none) instead of
+// seven.
+struct ReadbackSrc {
+  const Info* info;
+  const DevError* err;
+  const double *scal, *busy, *lsum;
+  const unsigned long long* mm;
+  const SelState* hs;
+};
+__global__ void readback_kernel(ReadbackSrc S, Readback* out) {
+  auto cp = [](void* d, const void* s, size_t bytes) {
+    for (size_t i = threadIdx.x; i < bytes / 4; i += blockDim.x)
+      static_cast<uint32_t*>(d)[i] = static_cast<const uint32_t*>(s)[i];
+  };
+  static_assert(sizeof(Info) % 4 == 0 && sizeof(DevError) % 4 == 0 && sizeof(SelState) % 4 == 0, "word copies");
+  cp(&out->info, S.info, sizeof(Info));
+  cp(&out->herr, S.err, sizeof(DevError));
+  cp(&out->hs, S.hs, sizeof(SelState));
+  if (threadIdx.x == 0) {
+    out->sc[0] = S.scal[0];
+    out->sc[1] = S.scal[1];
+    out->busy = *S.busy;
+    out->lsum = *S.lsum;
+    out->mm[0] = S.mm[0];
+    out->mm[1] = S.mm[1];
+  }
+}
+
 // the partition's verdict: a request error, or non-monotone arrivals
 static bool trace_input_error(const DevError& herr, const Info& info, TraceResult* R) {
   if (herr.packed != ~0ull) {
@@ -2183,7 +2263,7 @@ static bool trace_input_error(const DevError& herr, const Info& info, TraceResul
 }
 
 // finish(), simulator.hpp:283-301, from the read-back scalars.  p50/p99 are
-// interpolated_quantile (binning.hpp:98-104) over the ranks sel_init_kernel
+// interpolated_quantile (binning.hpp:98-104) over the ranks sel_init
 // selected.  Returns false when the one-launch selection overflowed and no
 // key array is at hand (a graph replay): the caller reruns the direct path.
 static bool trace_report(const TraceArgs& A, TraceResult* R, const Readback& rb, unsigned long long nc,
@@ -2365,7 +2445,15 @@ static void trace_run_impl(const TraceArgs& A, TraceResult* R, cudaStream_t s, T
       P.vec_ok = al(A.a, 16) && al(A.s, 16) && (!A.u_err || al(A.u_err, 16)) && (!A.pred || al(A.pred, 16)) &&
                  al(ws.pb8, 16) && (!A.req_true_bin || al(A.req_true_bin, 16));
     }
-    count_kernel<<<ntiles, PT, 0, s>>>(P);
+    {
+      int dev = 0, sms = 148;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      const uint32_t cg = std::min<uint32_t>(ntiles, (uint32_t)sms * 8);
+      if (k <= 8) count_kernel<1><<<cg, PT, 0, s>>>(P);
+      else if (k <= 16) count_kernel<2><<<cg, PT, 0, s>>>(P);
+      else count_kernel<4><<<cg, PT, 0, s>>>(P);
+    }
     tscan_kernel<<<k, TS_T, 0, s>>>(ws, ntiles, k, B);
     if (P.pred && P.tb_out) place_kernel<true><<<ntiles, PT, 0, s>>>(P);
     else place_kernel<false><<<ntiles, PT, 0, s>>>(P);
@@ -2812,15 +2900,15 @@ static void trace_run_impl(const TraceArgs& A, TraceResult* R, cudaStream_t s, T
     // one host round trip for everything the host reports
     Readback local{};
     Readback* rb = cap ? cap->rb : &local;
-    if (!host_sync) {
-      BB_CK(cudaMemcpyAsync(&rb->info, ws.info, sizeof(Info), cudaMemcpyDeviceToHost, s));
-      BB_CK(cudaMemcpyAsync(&rb->herr, ws.err, sizeof(DevError), cudaMemcpyDeviceToHost, s));
+    {
+      Readback* rdev = nullptr;  // the graph's pinned struct directly; else a device copy
+      if (cap) BB_CK(cudaHostGetDevicePointer((void**)&rdev, cap->rb, 0));
+      else BB_CK(pool.alloc((void**)&rdev, sizeof(Readback)));
+      readback_kernel<<<1, 128, 0, s>>>(ReadbackSrc{ws.info, ws.err, scal, busy_sum, lat_sum, kminmax, ds}, rdev);
+      note_launch();
+      BB_CK(cudaGetLastError());
+      if (!cap) BB_CK(cudaMemcpyAsync(rb, rdev, sizeof(Readback), cudaMemcpyDeviceToHost, s));
     }
-    BB_CK(cudaMemcpyAsync(rb->sc, scal, 16, cudaMemcpyDeviceToHost, s));
-    BB_CK(cudaMemcpyAsync(&rb->busy, busy_sum, 8, cudaMemcpyDeviceToHost, s));
-    BB_CK(cudaMemcpyAsync(&rb->lsum, lat_sum, 8, cudaMemcpyDeviceToHost, s));
-    BB_CK(cudaMemcpyAsync(rb->mm, kminmax, 16, cudaMemcpyDeviceToHost, s));
-    BB_CK(cudaMemcpyAsync(&rb->hs, ds, sizeof(SelState), cudaMemcpyDeviceToHost, s));
     if (capturing) {
       cudaGraph_t g = nullptr;
       capturing = false;
@@ -2912,7 +3000,13 @@ static bool trace_replay(TraceGraph& G, const TraceArgs& A, TraceResult* R, cuda
   return true;
 }
 
+static void trace_run_graph(const TraceArgs& A, TraceResult* R, cudaStream_t s);
 void trace_run(const TraceArgs& A, TraceResult* R, cudaStream_t s) {
+  trace_run_graph(A, R, s);
+  static const bool dbg = getenv("BB_TRACE_MS") != nullptr;
+  if (dbg) fprintf(stderr, "trace ms partition %.4f total %.4f\n", R->ms_partition, R->ms_total);
+}
+static void trace_run_graph(const TraceArgs& A, TraceResult* R, cudaStream_t s) {
   const bool graphable = s != nullptr && graphs_enabled() && !(A.max_batch_wait > 0) && !A.bat_formed &&
                          !A.bat_service && !A.bat_first && A.k >= 1 && A.k <= BB_TRACE_MAX_BINS;
   if (!graphable) return trace_run_impl(A, R, s, nullptr);
@@ -2937,7 +3031,7 @@ void trace_run(const TraceArgs& A, TraceResult* R, cudaStream_t s) {
   bool ok = true;
   for (int i = 0; i < 3 && ok; ++i)
     if (!G.ev[i]) ok = cudaEventCreate(&G.ev[i]) == cudaSuccess;
-  if (ok && !G.rb) ok = cudaMallocHost((void**)&G.rb, sizeof(Readback)) == cudaSuccess;
+  if (ok && !G.rb) ok = cudaHostAlloc((void**)&G.rb, sizeof(Readback), cudaHostAllocMapped | cudaHostAllocPortable) == cudaSuccess;
   if (ok && !G.edges) ok = cudaMalloc((void**)&G.edges, (BB_TRACE_MAX_BINS + 1) * 8) == cudaSuccess;
   if (ok && !G.conf) ok = cudaMalloc((void**)&G.conf, BB_TRACE_MAX_BINS * BB_TRACE_MAX_BINS * 8) == cudaSuccess;
   if (ok) ok = cudaMemcpyAsync(G.edges, A.edges, (size_t)(A.k + 1) * 8, cudaMemcpyDeviceToDevice, s) == cudaSuccess;
