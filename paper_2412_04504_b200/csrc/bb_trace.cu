@@ -1042,6 +1042,12 @@ struct PMap {
 __device__ __forceinline__ PMap pcompose(const PMap& x, const PMap& y) {  // y after x
   return PMap{x.i0 + ((x.i0 & 1) ? y.i1 : y.i0), x.i1 + ((x.i1 & 1) ? y.i0 : y.i1)};
 }
+// x * 2^n as ldexp rounds it, by one multiplication when 2^n is a normal
+// double (the library ldexp is a long branchy call)
+__device__ __forceinline__ double ldexp2(double x, int n) {
+  if (n >= -1022 && n <= 1023) return __dmul_rn(x, __longlong_as_double((long long)(n + 1023) << 52));
+  return ldexp(x, n);
+}
 __device__ __forceinline__ int binade(double v) { return (int)((__double_as_longlong(v) >> 52) & 0x7FF) - 1023; }
 
 // Is batch d a run head?  (needs d's code and the approximate D before/after)
@@ -1050,13 +1056,13 @@ __device__ __forceinline__ bool run_head(uint8_t code, double dprev, double dcur
   if (!(dprev > 0.0) || !(dcur > 0.0)) return true;
   const int e = binade(dcur);
   if (binade(dprev) != e) return true;
-  const double lo = ldexp(1.0, e), hi = ldexp(1.0, e + 1);
+  const double lo = ldexp2(1.0, e), hi = ldexp2(1.0, e + 1);
   return dprev < lo * (1.0 + 4 * tol_rel) || dcur > hi * (1.0 - 4 * tol_rel);
 }
 
 // map of one batch in binade e (q = floor(S/u), f = S/u - q exact)
 __device__ __forceinline__ PMap batch_map(double S, int e) {
-  const double x = ldexp(S, 52 - e);
+  const double x = ldexp2(S, 52 - e);
   const double qd = floor(x);
   const double f = x - qd;
   const long long q = (long long)qd;
@@ -1263,10 +1269,10 @@ __global__ void binade_chain_kernel(const double* __restrict__ R, const double* 
         *bad = 1;
         return;
       }
-      const long long a = (long long)ldexp(D, 52 - ri.e);
+      const long long a = (long long)ldexp2(D, 52 - ri.e);
       const long long al = a + ((a & 1) ? ri.p1 : ri.p0);
       if (al > (1ll << 53)) *bad = 1;
-      D = ldexp((double)al, ri.e - 52);
+      D = ldexp2((double)al, ri.e - 52);
     }
     const uint32_t nx = ri.last + 1;
     if (nx >= nb || ri.next_code == kSplit) return;
@@ -1296,13 +1302,13 @@ __global__ void binade_fill_kernel(const double* __restrict__ S, const double* _
     *bad = 1;
     return;
   }
-  const long long a = (long long)ldexp(Dh, 52 - e);
+  const long long a = (long long)ldexp2(Dh, 52 - e);
   const long long ap = (d - 1 == h) ? a : a + ((a & 1) ? p1[d - 1] : p0[d - 1]);
   const long long ad = a + ((a & 1) ? p1[d] : p0[d]);
-  const long long q = (long long)floor(ldexp(S[d], 52 - e));
+  const long long q = (long long)floor(ldexp2(S[d], 52 - e));
   if (ap + q >= (1ll << 53) || ad > (1ll << 53) || ap < (1ll << 52)) *bad = 1;
-  start[d] = ldexp((double)ap, e - 52);
-  finish[d] = ldexp((double)ad, e - 52);
+  start[d] = ldexp2((double)ap, e - 52);
+  finish[d] = ldexp2((double)ad, e - 52);
 }
 
 // the last value of a device-counted array (0 when empty)
