@@ -179,6 +179,9 @@ __device__ __forceinline__ uint32_t fold(Rep& R, uint64_t* __restrict__ slot, do
   return cnt;
 }
 
+#ifndef BB_QV256
+#define BB_QV256 1  // request-log stores as 256-bit vectors (sm_100 STG.E.256)
+#endif
 #ifndef BB_QWRITE
 #define BB_QWRITE 1  // 1: the first selection pass writes the latencies for the later ones
 #endif
@@ -471,11 +474,19 @@ __global__ void __launch_bounds__(kGenThreads, Q ? 2 : BB_GEN_MINB) gen_kernel(c
                 next_due = due < next_due ? due : next_due;
               }
             }
-            if (Q) {  // request log: arrivals and batch ids (16 B stores)
+            if (Q) {  // request log: arrivals and batch ids (full 32 B sectors)
               const size_t o = qlog_index(i);  // (i % 4 == 0: 4 requests stay in one run)
+#if BB_QV256
+#pragma unroll
+              for (int u = 0; u < U; u += 4)  // one 256-bit store (STG.E.256) per four arrivals
+                asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(q.A + o + u), "d"(at[u]),
+                             "d"(at[u + 1]), "d"(at[u + 2]), "d"(at[u + 3])
+                             : "memory");
+#else
 #pragma unroll
               for (int u = 0; u < U; u += 2)
                 *reinterpret_cast<double2*>(q.A + o + u) = make_double2(at[u], at[u + 1]);
+#endif
               // ids: a lane's eight consecutive ids are one 32 B sector; store
               // them together (half-sector stores cost several times more)
               static_assert(U == 4 || U % 8 == 0, "ids go out a full 32 B sector at a time");
@@ -483,8 +494,15 @@ __global__ void __launch_bounds__(kGenThreads, Q ? 2 : BB_GEN_MINB) gen_kernel(c
                 if ((i & 4u) == 0) {
                   idh = make_uint4(qid[0], qid[1], qid[2], qid[3]);
                 } else {
+#if BB_QV256
+                  asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(q.Id + o - 4),
+                               "r"(idh.x), "r"(idh.y), "r"(idh.z), "r"(idh.w), "r"(qid[0]), "r"(qid[1]),
+                               "r"(qid[2]), "r"(qid[3])
+                               : "memory");
+#else
                   *reinterpret_cast<uint4*>(q.Id + o - 4) = idh;
                   *reinterpret_cast<uint4*>(q.Id + o) = make_uint4(qid[0], qid[1], qid[2], qid[3]);
+#endif
                 }
               } else {
 #pragma unroll
