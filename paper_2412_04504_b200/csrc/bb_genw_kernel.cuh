@@ -159,6 +159,41 @@ __global__ void __launch_bounds__(kGenThreads, 2) genw_kernel(const __grid_const
     uint64_t ncomp = 0;
     uint32_t nb = 0;  // batch ids issued
     bool failed = false;
+    // Closings wait in a per-warp buffer (the selection's region, free until
+    // the end) and are served 32 at a time: every lane computes one batch's
+    // service (the log-normal's inverse CDF and exp no longer run with one
+    // lane active per step), then the Lindley chain walks them in request
+    // order -- the same fp64 steps in the same order.  Nothing in the
+    // arrival process depends on the server, so deferring is exact.
+    double* c_R = reinterpret_cast<double*>(wreg);   // closing time (= formation)
+    double* c_P = c_R + 64;                           // the bin's previous closing time
+    uint64_t* c_K = reinterpret_cast<uint64_t*>(c_P + 64);  // the batch's max key
+    uint32_t* c_I = reinterpret_cast<uint32_t*>(c_K + 64);  // its id
+    uint32_t c_n = 0;
+    auto serve_closings = [&]() {
+      __syncwarp();
+      for (uint32_t b0 = 0; b0 < c_n; b0 += 32) {
+        const uint32_t j = b0 + lane, m = c_n - b0 < 32 ? c_n - b0 : 32;
+        const bool v = j < c_n;
+        const double Rj = v ? c_R[j] : 0.0;
+        const double S = v ? svc_of_key_t<SVC>(svc, c_K[j]) : 0.0;
+        double fin = 0.0;
+        for (uint32_t c = 0; c < m; ++c) {
+          const double Sc = __shfl_sync(kQFull, S, c);
+          D = __dadd_rn(fmax(D, __shfl_sync(kQFull, Rj, c)), Sc);
+          busy += Sc;
+          if (lane == c) fin = D;
+        }
+        if (v) {
+          logF[c_I[j]] = fin;
+          const double lo = __dsub_rn(fin, Rj), hi = __dsub_rn(fin, c_P[j]);
+          lmin = lo < lmin ? lo : lmin;  // the closing member: the batch's smallest latency
+          lmax = hi > lmax ? hi : lmax;  // bounds the first member's (it arrived later)
+        }
+      }
+      c_n = 0;
+      __syncwarp();
+    };
     for (uint32_t base = 0; base < n; base += 32) {
       const uint32_t i = base + lane;
       const bool valid = i < n;
@@ -223,28 +258,22 @@ __global__ void __launch_bounds__(kGenThreads, 2) genw_kernel(const __grid_const
         logA[i] = ti;
         logI[i] = myid;
       }
-      // closings: every closing batch's service at once (one pass however
-      // many close), then the Lindley chain in request order
+      // closings: queued in request order (served 32 at a time, above)
       const uint32_t cm = __ballot_sync(kQFull, closing);
-      double S = 0.0, fin = 0.0;
-      if (closing) S = svc_of_key_t<SVC>(svc, bkey);
-      for (uint32_t m = cm; m; m &= m - 1) {
-        const int c = __ffs(m) - 1;
-        D = __dadd_rn(fmax(D, __shfl_sync(kQFull, ti, c)), __shfl_sync(kQFull, S, c));
-        busy += __shfl_sync(kQFull, S, c);
-        if (lane == (uint32_t)c) fin = D;
-      }
       ncomp += (uint64_t)B * __popc(cm);
       // the bin's previous closing: an earlier closing lane of the bin, else carried
       const uint32_t ecl = cm & peers & lt;
       const double prev_e = __shfl_sync(kQFull, ti, ecl ? 31 - __clz(ecl) : lane);
       const double prev_c = __shfl_sync(kQFull, oprev, pb ? pb - 1 : 0);
       if (closing) {
-        logF[myid] = fin;
-        const double lo = __dsub_rn(fin, ti), hi = __dsub_rn(fin, ecl ? prev_e : prev_c);
-        lmin = lo < lmin ? lo : lmin;  // the closing member: the batch's smallest latency
-        lmax = hi > lmax ? hi : lmax;  // bounds the first member's (it arrived later)
+        const uint32_t slot = c_n + __popc(cm & lt);
+        c_R[slot] = ti;
+        c_P[slot] = ecl ? prev_e : prev_c;
+        c_K[slot] = bkey;
+        c_I[slot] = myid;
       }
+      c_n += __popc(cm);
+      if (c_n >= 32) serve_closings();
       // carry each bin's open batch (its last member) and last closing time to the next step
       s_seen[lane] = 0;
       __syncwarp();
@@ -267,6 +296,7 @@ __global__ void __launch_bounds__(kGenThreads, 2) genw_kernel(const __grid_const
       }
       __syncwarp();
     }
+    if (!failed) serve_closings();
     double mk_out = 0.0, thr_out = 0.0, busy_out = 0.0, lat_out = 0.0;
     double q_p50 = BB_QNAN, q_p99 = BB_QNAN;
 #pragma unroll
