@@ -231,6 +231,7 @@ def main():
                     help="A/B only: skip the per-replication p50/p99 the reference computes")
     ap.add_argument("--no-ab", action="store_true", help="skip the without-quantiles A/B leg")
     ap.add_argument("--no-c5", action="store_true", help="skip the C5 large-run sample")
+    ap.add_argument("--no-c4", action="store_true", help="skip the C4 noisy-predictor grid")
     ap.add_argument("--dist-backend", default="nccl", help="nccl (default) or gloo for testing")
     args = ap.parse_args()
     if args.impl == "reference":
@@ -425,6 +426,11 @@ def main():
                 "note": "A/B only: p50/p99 left NaN, i.e. less work than the reference's run_point"}
         finally:
             bb.set_generated_quantiles(True)
+    if world == 1 and not args.no_c4:
+        try:
+            line["c4_grid"] = c4_measure(bb, torch, stream)
+        except Exception as e:  # secondary measurement; never fail the headline
+            line["c4_grid"] = {"error": repr(e)}
     if world == 1 and not args.no_c5:
         try:
             line["c5_sample"] = c5_measure(bb, torch, stream)
@@ -449,6 +455,40 @@ def main():
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def c4_measure(bb, torch, stream, reps=12_500, n=100_000):
+    """Secondary: BASELINE config 4 (noisy length predictor): k in {4, 8} x
+    symmetric misassignment p_e in {0, 0.05, ..., 0.30}, B = 32, U[1, 20]
+    lengths, lambda = 0.9 x the k-bin capacity, with exact per-replication
+    quantiles; 10^5 replicas across 8 GPUs is 12,500 per GPU per point.  One
+    shard launch per k (7 points), timed with CUDA events; the latency means
+    must be non-decreasing in p_e (common random numbers across p_e)."""
+    pes = [0.0, 0.05, 0.10, 0.15, 0.20, 0.25, 0.30]
+    svc = bb.ServiceSpec("uniform", 1.0, 20.0)
+    total_ms, monotone, per_k = 0.0, True, {}
+    for k in (4, 8):
+        lam = 0.9 * capacity(32, k, 1.0, 20.0)
+        pts = [bb.RunTemplate(arrival_rate=lam, n_requests=n, batch_size=32, bins=bb.BinRule(k=k),
+                              service=svc, error=bb.ErrorSpec("symmetric", pe)) for pe in pes]
+        rep = torch.zeros(6 * reps * len(pts), dtype=torch.float64, device="cuda")
+        bb.points_shard_device(pts, reps, 4, 0, reps, rep.data_ptr(), stream.cuda_stream)  # warm-up
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        bb.points_shard_device(pts, reps, 4, 0, reps, rep.data_ptr(), stream.cuda_stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        total_ms += e0.elapsed_time(e1)
+        res = bb.points_reduce_device(pts, reps, rep.data_ptr(), stream.cuda_stream)
+        lat = [p.latency_mean for p in res]
+        monotone &= all(b >= a for a, b in zip(lat, lat[1:]))
+        per_k[f"k{k}"] = {"latency_mean": lat, "latency_p99": [p.latency_p99 for p in res]}
+    req = 2 * len(pes) * reps * n
+    return {"workload": f"C4 grid: k in {{4,8}} x p_e {pes} symmetric, B=32, U[1,20], lambda=0.9 cap, "
+                        f"{reps} replications x {n} requests per point",
+            "value": req / (total_ms / 1e3), "unit": "requests/s", "ms": total_ms,
+            "latency_nondecreasing_in_p_e": monotone, **per_k}
 
 
 def c5_measure(bb, torch, stream, reps=148 * 16 * 32, n=1_000_000):
