@@ -869,7 +869,8 @@ cudaError_t launch_gen(const GenLaunch& L, cudaStream_t s) {
   if (per_thread) {
     // quantile mode may use most of HBM (a 10^5-request log is 0.9 MB per
     // thread); the S > 1 batch lists alone stay within 4 GiB as before
-    const uint64_t budget = Q ? gen_scratch_budget() : ((uint64_t)4 << 30);
+    const uint64_t budget =
+        Q ? gen_scratch_budget((uint64_t)grid * (per_thread + 1024) * kGenThreads) : ((uint64_t)4 << 30);
     const uint64_t max_grid = budget / ((per_thread + 1024) * kGenThreads);
     if (max_grid == 0) return cudaErrorMemoryAllocation;
     grid = (unsigned)(grid < max_grid ? grid : max_grid);
@@ -951,7 +952,7 @@ inline bool use_warp_mode(const GenLaunch& L) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const uint64_t per_lane = (((uint64_t)L.n_max + 31) & ~31ull) * 14 + (uint64_t)L.nf_max * 8;
   const uint64_t lanes = (uint64_t)sms * 2 * kGenThreads;  // the lane kernel's full grid
-  return per_lane * lanes > gen_scratch_budget();
+  return per_lane * lanes > gen_scratch_budget(per_lane * lanes);
 }
 
 template <int SVC, int ERR>

@@ -189,7 +189,9 @@ void gen_scratch_release(cudaStream_t s) {
   S.mu.unlock();
 }
 
-uint64_t gen_scratch_budget() {
+uint64_t gen_scratch_budget(uint64_t want) {
+  const uint64_t held = g_scratch[cur_dev()].bytes;
+  if (want && want <= held) return held;
   size_t free_b = 0, total_b = 0;
   if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) return 0;
   const uint64_t have = free_b + g_scratch[cur_dev()].bytes;

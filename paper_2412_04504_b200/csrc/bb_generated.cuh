@@ -71,8 +71,11 @@ struct GenLaunch {
 // order (acquire waits for the previous user's work; release records it).
 cudaError_t gen_scratch_acquire(size_t bytes, cudaStream_t s, void** out);
 void gen_scratch_release(cudaStream_t s);
-// Bytes the scratch may grow to (free HBM + what it already holds, less a reserve).
-uint64_t gen_scratch_budget();
+// Bytes the scratch may grow to (free HBM + what it already holds, less a
+// reserve).  want: what the caller needs; when the scratch already holds that
+// much, its size is returned without querying the device (cudaMemGetInfo
+// stalled the timed launches by 0.1-40 ms at random on the B200).
+uint64_t gen_scratch_budget(uint64_t want = 0);
 
 // Resolves key-space thresholds (bisection on the device sampler).
 cudaError_t gen_setup_thresholds(GenPoint* pts_dev, uint32_t n_points, cudaStream_t s);

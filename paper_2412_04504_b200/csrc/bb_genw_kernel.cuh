@@ -377,7 +377,7 @@ cudaError_t launch_genw(const GenLaunch& L, cudaStream_t s) {
   if (grid == 0) return cudaSuccess;
   const uint64_t q_n = ((uint64_t)L.n_max + 31) & ~31ull, q_nf = L.nf_max;
   const uint64_t per_warp = q_n * 14 + q_nf * 8 + 1024;
-  const uint64_t max_grid = gen_scratch_budget() / (per_warp * kGenWarps);
+  const uint64_t max_grid = gen_scratch_budget((uint64_t)grid * per_warp * kGenWarps + 4096) / (per_warp * kGenWarps);
   if (max_grid == 0) return cudaErrorMemoryAllocation;
   grid = (unsigned)std::min<uint64_t>(grid, max_grid);
   const uint64_t warps = (uint64_t)grid * kGenWarps;
