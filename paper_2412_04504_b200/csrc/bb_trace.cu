@@ -1606,6 +1606,10 @@ struct SelState {
   unsigned long long base, top;
   uint32_t shift, nt, need_collect, overflow, ncand;
   uint32_t bucket[kSelMax];
+  // direct: the level-1 target buckets' keys fit the candidate buffer, so the
+  // level-2 pass also lists them (ncand1 of them) and the collect pass reads
+  // that list instead of every key
+  uint32_t direct, ncand1;
 };
 
 // interpolated_quantile's ranks (binning.hpp:98-104) from the completed count
@@ -1631,6 +1635,8 @@ __global__ void sel_init_kernel(SelState* S, const unsigned long long* kminmax, 
   S->shift = bits > HBITS ? (uint32_t)(bits - HBITS) : 0u;
   S->ncand = 0;
   S->overflow = 0;
+  S->direct = 0;
+  S->ncand1 = 0;
 }
 
 __global__ void sel_hist_kernel(const unsigned long long* __restrict__ key, uint32_t m,
@@ -1726,14 +1732,15 @@ __global__ void __launch_bounds__(1024) sel_find_kernel(SelState* S, const uint3
     }
     __syncthreads();
   }
-  if (t == 0) S->overflow = need > cap;
+  if (t == 0) S->direct = need <= cap;
 }
 
 // level 2 over the full key array: every unresolved target's bucket split
 // into 2048 sub-buckets at once (per-target shared histograms)
 constexpr int kSub = 2048;
 __global__ void sel_hist2_kernel(const unsigned long long* __restrict__ key, uint32_t m,
-                                 const SelState* S, uint32_t* __restrict__ hist2) {
+                                 SelState* S, uint32_t* __restrict__ hist2,
+                                 unsigned long long* __restrict__ out, uint32_t cap) {
   __shared__ uint32_t h[kSelMax][kSub];
   __shared__ unsigned long long s_lo[kSelMax], s_hi[kSelMax];
   __shared__ uint32_t s_sh[kSelMax];
@@ -1749,10 +1756,19 @@ __global__ void sel_hist2_kernel(const unsigned long long* __restrict__ key, uin
   }
   __syncthreads();
   if (!S->need_collect) return;
+  const bool direct = S->direct != 0;
   for_keys(key, m, [&](unsigned long long v) {
+    bool in = false;
 #pragma unroll
     for (int q = 0; q < kSelMax; ++q)
-      if (v >= s_lo[q] && v <= s_hi[q]) atomicAdd(&h[q][(uint32_t)((v - s_lo[q]) >> s_sh[q])], 1u);
+      if (v >= s_lo[q] && v <= s_hi[q]) {
+        atomicAdd(&h[q][(uint32_t)((v - s_lo[q]) >> s_sh[q])], 1u);
+        in = true;
+      }
+    if (direct && in) {  // the level-1 candidates (the union of the target buckets)
+      const uint32_t slot = atomicAdd(&S->ncand1, 1u);
+      if (slot < cap) out[slot] = v;
+    }
   });
   __syncthreads();
   for (int i = threadIdx.x; i < kSelMax * kSub; i += blockDim.x)
@@ -1799,8 +1815,13 @@ __global__ void __launch_bounds__(1024) sel_find2_kernel(SelState* S, const uint
 }
 
 __global__ void sel_collect_kernel(const unsigned long long* __restrict__ key, uint32_t m,
-                                   SelState* S, unsigned long long* __restrict__ out, uint32_t cap) {
+                                   const unsigned long long* __restrict__ l1, SelState* S,
+                                   unsigned long long* __restrict__ out, uint32_t cap) {
   if (!S->need_collect || S->overflow) return;
+  if (S->direct) {  // the level-1 candidates listed by the level-2 pass
+    key = l1;
+    m = S->ncand1;
+  }
   unsigned long long lo[kSelMax], hi[kSelMax];
   const uint32_t nt = S->nt;
   for (uint32_t q = 0; q < kSelMax; ++q) {
@@ -2887,13 +2908,15 @@ static void trace_run_impl(const TraceArgs& A, TraceResult* R, cudaStream_t s, T
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
       sel_init_kernel<<<1, 1, 0, s>>>(ds, kminmax, ws.info);
       sel_hist_kernel<<<sms * 4, 256, 0, s>>>(keys, n, ds, dh);
-      sel_find_kernel<<<1, 1024, 0, s>>>(ds, dh, 0xFFFFFFFFu);
+      sel_find_kernel<<<1, 1024, 0, s>>>(ds, dh, cap);
       uint32_t* dh2;
       BB_CK(pool.alloc((void**)&dh2, (size_t)kSelMax * kSub * 4));
       BB_CK(cudaMemsetAsync(dh2, 0, (size_t)kSelMax * kSub * 4, s));
-      sel_hist2_kernel<<<sms * 2, 512, 0, s>>>(keys, n, ds, dh2);
+      unsigned long long* dl1;
+      BB_CK(pool.alloc((void**)&dl1, (size_t)cap * 8));
+      sel_hist2_kernel<<<sms * 2, 512, 0, s>>>(keys, n, ds, dh2, dl1, cap);
       sel_find2_kernel<<<1, 1024, 0, s>>>(ds, dh2, cap);
-      sel_collect_kernel<<<sms * 4, 256, 0, s>>>(keys, n, ds, dc, cap);
+      sel_collect_kernel<<<sms * 4, 256, 0, s>>>(keys, n, dl1, ds, dc, cap);
       sel_refine_kernel<<<1, 1024, 0, s>>>(ds, dc);
       note_launch(7);
       BB_CK(cudaGetLastError());
