@@ -1443,7 +1443,10 @@ struct QArgs {
 };
 
 
-constexpr int RQ_T = 256, RQ_E = 4;  // request pass: threads, requests per thread
+#ifndef BB_RQ_E
+#define BB_RQ_E 4
+#endif
+constexpr int RQ_T = 256, RQ_E = BB_RQ_E;  // request pass: threads, requests per thread
 __global__ void __launch_bounds__(RQ_T) request_kernel(QArgs Q) {
   __shared__ double s_sum[RQ_T / 32];
   __shared__ unsigned long long s_min[RQ_T / 32], s_max[RQ_T / 32];
