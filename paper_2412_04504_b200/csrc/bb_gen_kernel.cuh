@@ -870,8 +870,8 @@ cudaError_t launch_gen(const GenLaunch& L, cudaStream_t s) {
     // quantile mode may use most of HBM (a 10^5-request log is 0.9 MB per
     // thread); the S > 1 batch lists alone stay within 4 GiB as before
     const uint64_t budget =
-        Q ? gen_scratch_budget((uint64_t)grid * (per_thread + 1024) * kGenThreads) : ((uint64_t)4 << 30);
-    const uint64_t max_grid = budget / ((per_thread + 1024) * kGenThreads);
+        Q ? gen_scratch_budget((uint64_t)grid * kGenThreads * per_thread + 2048) : ((uint64_t)4 << 30);
+    const uint64_t max_grid = budget / (per_thread * kGenThreads);  // (the budget keeps its own reserve)
     if (max_grid == 0) return cudaErrorMemoryAllocation;
     grid = (unsigned)(grid < max_grid ? grid : max_grid);
     const uint64_t slots = (uint64_t)grid * kGenThreads;

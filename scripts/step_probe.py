@@ -18,6 +18,9 @@ pts = bench.sweep_points(100000)
 tpl = [bb.RunTemplate(arrival_rate=p["lam"], n_requests=p["n"], batch_size=p["B"], bins=bb.BinRule(k=p["k"]),
                       service=bb.ServiceSpec("linear", 1.0, 1024.0, intercept=bench.A_INTERCEPT,
                                              slope=bench.B_SLOPE)) for p in pts]
+sampler = bench.ClockSampler(0) if os.environ.get("PROBE_CLOCKS") else None
+if sampler:
+    sampler.__enter__()
 for R in [int(x) for x in sys.argv[1:]] or [2000, 10000]:
     block = torch.empty(6 * len(tpl) * R, dtype=torch.float64, device=dev)
     for it in range(4):
@@ -35,3 +38,5 @@ for R in [int(x) for x in sys.argv[1:]] or [2000, 10000]:
         print(f"R={R} it={it} step_ms={ev[0].elapsed_time(ev[2]):.2f} shard_dev_ms={ev[0].elapsed_time(ev[1]):.2f} "
               f"reduce_dev_ms={ev[1].elapsed_time(ev[2]):.2f} kernel_ms={bb.last_kernel_ms()[0]:.2f} "
               f"host_shard_ms={(t1-t0)*1e3:.2f} host_reduce_ms={(t2-t1)*1e3:.2f}", flush=True)
+if sampler:
+    sampler.__exit__(None, None, None)
